@@ -1,0 +1,413 @@
+#!/usr/bin/env python
+"""bench.py — EvoformerAttention fwd+bwd TFLOP/s & peak memory on B200 (BASELINE.json metric).
+
+One step = forward + backward of DS4Sci_EvoformerAttention over the whole
+workload (all rows, all heads) with mask bias1 and pair bias2, dBias2 reduced
+over rows (in-kernel, then NCCL all-reduce across ranks when N > 1).
+Default workload: configs[3] of BASELINE.json — OpenFold finetune MSA row
+attention N_seq=512 N_res=384 H=8 D=32 bf16 — the configuration the north-star
+target (>=50% of dense bf16 peak on 1 B200) is quoted on. --config c1..c5
+selects the others. Multi-GPU: rows sharded over ranks (strong scaling).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config c4] [--impl ours|reference]
+  torchrun --nproc-per-node N bench.py --gpus N ...
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+CONFIGS = {
+    # name: (Bo, N, L, H, D, dtype, description)
+    "c1": (1, 32, 64, 8, 32, "f32", "MSA row attention mask+pair bias fp32, N_seq=32 N_res=64 H=8 D=32"),
+    "c2": (1, 128, 256, 8, 32, "bf16", "OpenFold initial-training MSA row attention bf16, N_seq=128 N_res=256 H=8 D=32"),
+    "c3": (1, 384, 384, 4, 32, "bf16", "Triangle attention bf16, N_res=384 H=4 D=32, mask+pair bias"),
+    "c4": (1, 512, 384, 8, 32, "bf16", "OpenFold finetune MSA row attention bf16, N_seq=512 N_res=384 H=8 D=32"),
+    "c5": (1, 2048, 2048, 4, 32, "bf16", "Long-protein triangle attention bf16, N_res=2048 H=4 D=32"),
+}
+METRIC = "EvoformerAttention fwd+bwd TFLOP/s & peak mem, OpenFold shapes, 1-8 B200"
+UNIT = "TFLOP/s"
+
+
+def flops(B, L, H, D):
+    """FlashAttention convention 14*B*H*L^2*D per fwd+bwd: fwd 4, bwd 10."""
+    return 14.0 * B * H * L * L * D
+
+
+def ideal_bytes(B, L, H, D, elem=2):
+    """SURVEY §8d byte convention: 24N (bf16 I/O) + 16BHL (LSE, delta) + 16HL^2 (bias2, dbias2) + 4BL."""
+    n = B * L * H * D
+    return (12 * elem) * n + 16 * B * H * L + 16 * H * L * L + 4 * B * L
+
+
+def peaks():
+    p = {"hbm_gbs": 6534.5, "bf16_tflops": 1667.1, "bf16_tflops_sustained": 1376.6, "source": "fallback"}
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            m = json.load(f)
+        p.update({k: m[k] for k in ("hbm_gbs", "bf16_tflops", "bf16_tflops_sustained") if k in m})
+        p["source"] = "measured"
+    except Exception:
+        pass
+    return p
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled DURING the timed region."""
+
+    FIELDS = "clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap"
+
+    def __init__(self, gpu_index: int):
+        self.gpu = gpu_index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "50", "-i", str(self.gpu)], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL,
+                text=True)
+            self._t = threading.Thread(target=self._read, daemon=True)
+            self._t.start()
+            time.sleep(0.3)
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *exc):
+        if self.proc:
+            time.sleep(0.1)
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 6:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = float(parts[1])
+            except ValueError:
+                continue
+            for n, p in zip(names, parts[2:]):
+                if p.lower() == "active":
+                    reasons.add(n)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        loaded = [x for x in sm if x > 0.5 * (mx or 1)] or sm
+        return {"sm_mhz": statistics.median(loaded), "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def make_inputs(cfg, rows, device, seed=7):
+    """Synthetic OpenFold-shaped inputs: U[-1,1) rounded once to the
+    compute dtype; mask bias1 in {0,-1e9} at 10% (key 0 never masked)."""
+    import torch
+
+    Bo, Nr, L, H, D, dt, _ = cfg
+    dtype = {"f32": torch.float32, "bf16": torch.bfloat16}[dt]
+    g = torch.Generator(device=device).manual_seed(seed)
+    lo, hi = rows
+    u = lambda *s: (torch.rand(*s, generator=g, device=device) * 2 - 1)
+    # generate the full tensors' row range deterministically (same values on every rank)
+    full = lambda: u(Bo, Nr, L, H, D)
+    q, k, v, do = full(), full(), full(), full()
+    m = torch.rand(Bo, Nr, 1, 1, L, generator=g, device=device) < 0.1
+    m[..., 0] = False
+    b1 = torch.where(m, -1e9, 0.0)
+    b2 = u(Bo, 1, H, L, L)
+    sl = lambda t: t[:, lo:hi].contiguous()
+    out = [sl(q), sl(k), sl(v), sl(do), sl(b1), b2]
+    del q, k, v, do
+    return [t.to(dtype) for t in out]
+
+
+def cpu_baseline(cfg, sample_rows, threads):
+    """Reference attn_forward_tiled + attn_backward_tiled (oracle/_ref, the
+    reference's own sources) in F32 on `sample_rows` rows, row-sharded over
+    `threads` host threads. Falls back to the C restatement if _ref is absent."""
+    import numpy as np
+    import torch
+
+    from oracle import oracle as O
+
+    Bo, Nr, L, H, D, dt, _ = cfg
+    q, k, v, do, b1, b2 = make_inputs(cfg, (0, sample_rows), "cpu")
+    f = lambda t: t.float().numpy().reshape(-1, L, H, D) if t.dim() == 5 and t.shape[-1] == D else t.float().numpy()
+    qn, kn, vn, don = (f(t) for t in (q, k, v, do))
+    b2n = b2.float().numpy().reshape(H, L, L)
+    t0 = time.perf_counter()
+    if O.ref_available():
+        O.ref_threaded_f32(qn, kn, vn, b2n, don, threads)
+        kind = "reference"
+    else:
+        p = O.Problem(sample_rows, L, H, D)
+        O.fwd_bwd_threaded(p, threads, qn, kn, vn, don, b1.float().numpy().reshape(-1, L), b2n)
+        kind = "port"
+    dt_s = time.perf_counter() - t0
+    tf = flops(sample_rows, L, H, D) / dt_s / 1e12
+    return {"value": tf, "unit": UNIT, "cores": threads, "kind": kind,
+            "sample": f"{sample_rows} of {Bo * Nr} rows of {cfg[6]}, F32 tiled fwd+bwd (tile 64,64,1), "
+                      f"{dt_s:.2f} s; mask bias omitted (the reference has no bias1)" if kind == "reference"
+                      else f"{sample_rows} rows, oracle port, {dt_s:.2f} s"}
+
+
+def run_reference_arm(args, cfg):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    threads = os.cpu_count() or 1
+    Bo, Nr, L, H, D, dt, desc = cfg
+    # bounded sample per step: one row per host thread, shrunk so that the
+    # whole (warmup + steps) run stays within ~4 minutes
+    sample = min(Bo * Nr, threads)
+    first = cpu_baseline(cfg, sample, threads)
+    per_step = flops(sample, L, H, D) / (first["value"] * 1e12)
+    budget = 240.0 / max(1, args.steps + args.warmup)
+    if per_step > budget:
+        sample = max(1, int(sample * budget / per_step))
+        threads = min(threads, sample)
+    for _ in range(args.warmup - 1):
+        cpu_baseline(cfg, sample, threads)
+    vals = [cpu_baseline(cfg, sample, threads) for _ in range(args.steps)]
+    v = statistics.median(x["value"] for x in vals)
+    ms = flops(sample, L, H, D) / (v * 1e12) * 1e3
+    line = {"metric": METRIC, "value": v, "unit": UNIT, "n_gpus": 0, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": {"workload": desc, "Bo": Bo, "N": Nr, "L": L, "H": H, "D": D,
+                       "parallelism": f"cpu_threads{threads}"},
+            "impl": "reference",
+            "cpu_baseline": {"value": v, "unit": UNIT, "cores": threads, "kind": vals[0]["kind"],
+                             "sample": vals[0]["sample"]},
+            "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=100)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--config", default="c4", choices=sorted(CONFIGS))
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--e2e-steps", type=int, default=5)
+    ap.add_argument("--all-configs", action="store_true", help="also time c1..c5 and attach them")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+    cfg = CONFIGS[args.config]
+    if args.impl == "reference":
+        run_reference_arm(args, cfg)
+        return
+
+    import torch
+    import torch.distributed as dist
+
+    import paper_2310_04610_b200 as E
+    from paper_2310_04610_b200.sharded import shard_rows, sharded_fwd_bwd
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+
+    Bo, Nr, L, H, D, dt, desc = cfg
+    lo, hi = shard_rows(Nr, world, rank)
+    q, k, v, do, b1, b2 = (t.to(dev) for t in make_inputs(cfg, (lo, hi), dev))
+    B_local = Bo * (hi - lo)
+
+    def step():
+        return sharded_fwd_bwd(q, k, v, do, b1, b2)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    # ---- warm-up + launch count
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    E.evoformer_attention_forward(q, k, v, b1, b2)
+    n_fwd = E.last_launch_count()
+    o, lse = E.evoformer_attention_forward(q, k, v, b1, b2)
+    E.evoformer_attention_backward(do, q, k, v, o, lse, b1, b2, need_dbias1=True)
+    n_bwd = E.last_launch_count()
+    path = E.resolved_path(q, b1, b2)
+
+    # ---- peak memory of one fwd+bwd beyond the I/O tensors
+    torch.cuda.synchronize()
+    io = [q, k, v, do, b1, b2]
+    base = torch.cuda.memory_allocated()
+    torch.cuda.reset_peak_memory_stats()
+    r = step()
+    torch.cuda.synchronize()
+    outs = sum(t.numel() * t.element_size() for t in (r.o, r.dq, r.dk, r.dv) if t is not None)
+    outs += sum(t.numel() * t.element_size() for t in (r.dbias1, r.dbias2) if t is not None)
+    peak_extra = torch.cuda.max_memory_allocated() - base - outs
+    del r
+
+    # ---- timed region: K steps, barrier + sync on both sides, CUDA events
+    stream = torch.cuda.current_stream()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        barrier()
+        torch.cuda.synchronize()
+        ev0.record(stream)
+        for _ in range(args.steps):
+            step()
+        ev1.record(stream)
+        torch.cuda.synchronize()
+        barrier()
+    ms = ev0.elapsed_time(ev1) / args.steps
+    t = torch.tensor([ms], device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms = float(t.item())
+    total_flops = flops(Bo * Nr, L, H, D)
+    value = total_flops / (ms * 1e-3) / 1e12
+
+    # ---- per-kernel timing (forward call, backward call) on the launching stream
+    def time_call(fn, n):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize()
+        a.record(stream)
+        for _ in range(n):
+            fn()
+        b.record(stream)
+        torch.cuda.synchronize()
+        return a.elapsed_time(b) / n
+
+    o, lse = E.evoformer_attention_forward(q, k, v, b1, b2)
+    nk = max(10, args.steps // 2)
+    fwd_ms = time_call(lambda: E.evoformer_attention_forward(q, k, v, b1, b2), nk)
+    bwd_ms = time_call(lambda: E.evoformer_attention_backward(do, q, k, v, o, lse, b1, b2,
+                                                              need_dbias1=True), nk)
+    pk = peaks()
+    f_fwd = 4.0 * B_local * H * L * L * D
+    f_bwd = 10.0 * B_local * H * L * L * D
+    dom = ("bwd", f_bwd, bwd_ms) if bwd_ms >= fwd_ms else ("fwd", f_fwd, fwd_ms)
+    achieved = dom[1] / (dom[2] * 1e-3) / 1e12
+    traffic = None
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
+            tr = json.load(f).get(f"{args.config}_{dom[0]}_{path}")
+            traffic = tr
+    except Exception:
+        pass
+    roofline = {"bound": "tensor", "achieved": achieved, "peak": pk["bf16_tflops"], "unit": "TFLOP/s",
+                "frac": achieved / pk["bf16_tflops"], "traffic": traffic, "kernel": f"{dom[0]} ({path})",
+                "peak_source": pk["source"],
+                "kernels": {"fwd": {"ms": fwd_ms, "tflops": f_fwd / fwd_ms / 1e9},
+                            "bwd": {"ms": bwd_ms, "tflops": f_bwd / bwd_ms / 1e9}},
+                "step_roofline_frac": (max(total_flops / world / (pk["bf16_tflops"] * 1e12),
+                                           ideal_bytes(B_local, L, H, D) / (pk["hbm_gbs"] * 1e9))
+                                       / (ms * 1e-3))}
+
+    # ---- end to end through the public API with pinned host buffers
+    host_in = [t.cpu().pin_memory() for t in (q, k, v, do, b1, b2)]
+    dev_in = [torch.empty_like(t) for t in (q, k, v, do, b1, b2)]
+    r = step()
+    host_out = [torch.empty(t.shape, dtype=t.dtype, pin_memory=True) for t in (r.dq, r.dk, r.dv, r.dbias2)]
+    h2d = sum(t.numel() * t.element_size() for t in host_in)
+    d2h = sum(t.numel() * t.element_size() for t in host_out)
+
+    def e2e_step():
+        for hs, ds in zip(host_in, dev_in):
+            ds.copy_(hs, non_blocking=True)
+        rr = sharded_fwd_bwd(*dev_in)
+        for hd, t_ in zip(host_out, (rr.dq, rr.dk, rr.dv, rr.dbias2)):
+            hd.copy_(t_, non_blocking=True)
+
+    e2e_step()
+    torch.cuda.synchronize()
+    barrier()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record(stream)
+    for _ in range(args.e2e_steps):
+        e2e_step()
+    b.record(stream)
+    torch.cuda.synchronize()
+    barrier()
+    e2e_ms = a.elapsed_time(b) / args.e2e_steps
+    t = torch.tensor([e2e_ms], device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    e2e_ms = float(t.item())
+
+    extra = {}
+    if args.all_configs and world == 1:
+        for name, c in CONFIGS.items():
+            if name == args.config:
+                continue
+            qq, kk, vv, dd, bb1, bb2 = (x.to(dev) for x in make_inputs(c, (0, c[1]), dev))
+            for _ in range(3):
+                sharded_fwd_bwd(qq, kk, vv, dd, bb1, bb2)
+            n = 20 if name != "c5" else 3
+            mm = time_call(lambda: sharded_fwd_bwd(qq, kk, vv, dd, bb1, bb2), n)
+            extra[name] = {"ms_per_step": mm, "tflops": flops(c[0] * c[1], c[2], c[3], c[4]) / mm / 1e9,
+                           "path": E.resolved_path(qq, bb1, bb2)}
+            del qq, kk, vv, dd, bb1, bb2
+            torch.cuda.empty_cache()
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        try:
+            th = os.cpu_count() or 1
+            cpu = cpu_baseline(cfg, max(th, (Bo * Nr) // 64) if args.config != "c5" else 2, th)
+        except Exception as e:  # reported, never silently substituted
+            cpu = {"value": None, "unit": UNIT, "cores": 0, "kind": "unavailable", "sample": repr(e)}
+
+    if rank == 0:
+        naive = 3 * H * Bo * Nr * L * L * (2 if dt == "bf16" else 4)
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": dt, "data": "synthetic",
+            "config": {"workload": desc, "config": args.config, "Bo": Bo, "N": Nr, "L": L, "H": H,
+                       "D": D, "biases": "mask bias1 [Bo,N,1,1,L] + pair bias2 [Bo,1,H,L,L]",
+                       "parallelism": f"rows_sharded_dp{world}", "kernel_path": path,
+                       "l2": "inputs+outputs larger than L2 (no flush needed)" if ideal_bytes(Bo * Nr, L, H, D) > 126e6
+                       else "working set smaller than L2 (not flushed)"},
+            "peak_mem": {"extra_bytes_per_rank": int(peak_extra), "naive_logits_bytes": naive,
+                         "o_l_plan_bytes": 8 * B_local * H * L + 4 * H * L * L},
+            "roofline": roofline,
+            "cpu_baseline": cpu,
+            "e2e": {"value": total_flops / (e2e_ms * 1e-3) / 1e12, "unit": UNIT, "ms_per_step": e2e_ms,
+                    "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
+            "gpu_launches": (n_fwd + n_bwd) * args.steps,
+            "clocks": clk.summary(),
+        }
+        if extra:
+            line["other_configs"] = extra
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,105 @@
+/* evoattn.h — C-ABI of the B200-native Evoformer attention (DS4Sci_EvoformerAttention).
+ *
+ * This is the drop-in boundary: plain pointers and sizes, no torch types.
+ * Each entry point replaces one operator of the reference's API:
+ *
+ *   evo_attn_fwd   <- evomem::attn_forward_tiled
+ *                     /root/reference/proj/core/include/evomem/attention_tiled.hpp:85-86
+ *                     (implementation attention_tiled.cpp:57-180)
+ *   evo_attn_bwd   <- evomem::attn_backward_tiled
+ *                     attention_tiled.hpp:94-97 (attention_tiled.cpp:182-340)
+ *   evo_attn_*_workspace_size  — device scratch the caller owns (the
+ *                     reference's "tiled/work", "tiled/stats", "tiled/delta"
+ *                     ledger allocations, attention_tiled.cpp:79-97, 229).
+ *   evo_status     <- the reference's exception taxonomy errors.hpp:15-36
+ *                     (ValidationError / NumericError / UsageError).
+ *
+ * Shapes follow DeepSpeed's DS4Sci_EvoformerAttention (north star):
+ *   q, k, v, o, do, dq, dk, dv : [Bo, N, L, H, D]   (== reference (B, L, H, D), B = Bo*N)
+ *   bias1 (mask)  / dbias1     : [Bo, N, 1, 1, L]   (optional; not in the reference)
+ *   bias2 (pair)  / dbias2     : [Bo, 1, H, L, L]   (optional; reference `bias` (H, L, L) is Bo == 1)
+ *   lse                         : [Bo*N, H, L] fp32, natural-log units
+ *                                 (reference RowStats is (H, B, L); same values)
+ * All pointers are DEVICE pointers owned by the caller; nothing is allocated
+ * inside. Calls are stream-ordered and asynchronous. Contiguous row-major.
+ */
+#ifndef EVOATTN_H
+#define EVOATTN_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct CUstream_st* evo_stream_t; /* == cudaStream_t */
+
+typedef enum {
+  EVO_OK = 0,
+  EVO_ERR_VALIDATION = 1, /* ValidationError: shapes, dtypes, missing inputs, bad workspace */
+  EVO_ERR_NUMERIC = 2,    /* NumericError: non-finite scale */
+  EVO_ERR_USAGE = 3,      /* UsageError: API misuse (null descriptor, no device) */
+  EVO_ERR_CUDA = 4,       /* a CUDA launch / runtime failure */
+  EVO_ERR_UNSUPPORTED = 5 /* shape outside the kernels' envelope (e.g. D > 64 on fp32) */
+} evo_status;
+
+typedef enum { EVO_F32 = 0, EVO_BF16 = 1, EVO_F16 = 2 } evo_dtype;
+
+/* Kernel family selection. AUTO picks tcgen05 (sm_100a tensor cores) for
+ * bf16/f16 with D in {16, 32, 64} and the SIMT (FFMA) kernels otherwise
+ * (fp32 must not use TF32: it fails the 1e-4 parity bar). */
+typedef enum { EVO_PATH_AUTO = 0, EVO_PATH_SIMT = 1, EVO_PATH_TCGEN05 = 2 } evo_path;
+
+typedef struct {
+  int64_t Bo;        /* outer batch of the pair bias */
+  int64_t N;         /* rows per outer batch (MSA rows / triangle start nodes) */
+  int64_t L;         /* attended axis */
+  int64_t H;         /* heads */
+  int64_t D;         /* head dim */
+  evo_dtype dtype;   /* dtype of q, k, v, o, do, dq, dk, dv, bias1, bias2 */
+  double scale;      /* logit scale (reference default 1/sqrt(D), attention.cpp:43-45) */
+  int has_bias1;     /* mask bias present */
+  int has_bias2;     /* pair bias present */
+  evo_dtype dbias_dtype; /* dtype of dbias1/dbias2 outputs: EVO_F32 = the reference's
+                            UpcastF32 policy (attention_tiled.cpp:218-223), or == dtype */
+  evo_path path;
+} evo_attn_desc;
+
+size_t evo_attn_fwd_workspace_size(const evo_attn_desc* desc);
+size_t evo_attn_bwd_workspace_size(const evo_attn_desc* desc);
+
+/* Forward: o = softmax(scale*q k^T + bias1 + bias2) v, lse = logsumexp per row.
+ * bias1/bias2 may be NULL when the descriptor says absent. */
+evo_status evo_attn_fwd(const evo_attn_desc* desc, const void* q, const void* k, const void* v,
+                        const void* bias1, const void* bias2, void* o, float* lse,
+                        void* workspace, size_t workspace_bytes, evo_stream_t stream);
+
+/* Backward by recomputation from lse. dbias1/dbias2 may be NULL (not wanted).
+ * dbias2 is the batch-axis sum of dS (reduced inside the kernels); when
+ * accumulate_dbias != 0 it is ADDED to the caller's dbias2/dbias1 buffers
+ * (dbias_dtype must be EVO_F32), which lets a row-sharded launcher
+ * accumulate partial sums before its all-reduce. */
+evo_status evo_attn_bwd(const evo_attn_desc* desc, const void* dout, const void* q, const void* k,
+                        const void* v, const void* bias1, const void* bias2, const void* o,
+                        const float* lse, void* dq, void* dk, void* dv, void* dbias1,
+                        void* dbias2, int accumulate_dbias, void* workspace,
+                        size_t workspace_bytes, evo_stream_t stream);
+
+/* Which kernel family AUTO resolves to for this descriptor (EVO_PATH_SIMT or
+ * EVO_PATH_TCGEN05); negative if the descriptor is invalid. */
+int evo_attn_resolved_path(const evo_attn_desc* desc);
+
+/* Number of kernel launches the last fwd / bwd call issued on this thread. */
+int evo_attn_last_launch_count(void);
+
+/* Message of the last error on this thread ("" if none). */
+const char* evo_attn_last_error(void);
+
+/* Library version string, e.g. "evoattn 0.1 sm_100a". */
+const char* evo_attn_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* EVOATTN_H */

@@ -1,0 +1,70 @@
+"""Row-sharding launcher: one process per GPU, rows of the batch axis split
+contiguously over ranks, NCCL all-reduce of the pair-bias gradient only.
+
+Rows (MSA rows / triangle start nodes) are independent for O, LSE, dQ, dK, dV
+(attention_tiled.cpp:83-177, 254-330); the only coupling is dBias2 =
+sum_b dS (attention_tiled.cpp:318-323), the broadcast-reverse sum. Each rank
+reduces its rows inside the kernels into an fp32 partial; the launcher then
+all-reduces that partial (sum, fp32) over NVLink. bias1 is per-row, so its
+gradient needs no communication.
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass
+from typing import Optional, Tuple
+
+import torch
+import torch.distributed as dist
+
+from .evoformer_attention import evoformer_attention_backward, evoformer_attention_forward
+
+
+def shard_rows(n_rows: int, world: int, rank: int) -> Tuple[int, int]:
+    """Contiguous near-equal split of [0, n_rows): rank r gets [lo, hi)."""
+    if world < 1 or not 0 <= rank < world:
+        raise ValueError("bad world/rank")
+    lo = n_rows * rank // world
+    hi = n_rows * (rank + 1) // world
+    return lo, hi
+
+
+@dataclass
+class ShardedStep:
+    o: torch.Tensor
+    lse: torch.Tensor
+    dq: torch.Tensor
+    dk: torch.Tensor
+    dv: torch.Tensor
+    dbias1: Optional[torch.Tensor]
+    dbias2: Optional[torch.Tensor]
+
+
+def sharded_fwd_bwd(q, k, v, dout, bias1, bias2, group=None, head_chunks: int = 1,
+                    dbias_dtype: torch.dtype = torch.float32) -> ShardedStep:
+    """Forward + backward on this rank's row shard, dBias2 all-reduced.
+
+    q/k/v/dout/bias1 are this rank's rows ([Bo, n_local, L, H, D]); bias2 is
+    the full pair bias. `head_chunks` > 1 issues the all-reduce per head group
+    on a side stream so it overlaps the next group's compute.
+    """
+    o, lse = evoformer_attention_forward(q, k, v, bias1, bias2)
+    world = dist.get_world_size(group) if dist.is_initialized() else 1
+    dq, dk, dv, db1, db2 = evoformer_attention_backward(
+        dout, q, k, v, o, lse, bias1, bias2, need_dbias1=bias1 is not None,
+        need_dbias2=bias2 is not None, dbias_dtype=torch.float32)
+    if db2 is not None and world > 1:
+        dist.all_reduce(db2, op=dist.ReduceOp.SUM, group=group)
+    if db2 is not None and dbias_dtype != torch.float32:
+        db2 = db2.to(dbias_dtype)
+    if db1 is not None and dbias_dtype != torch.float32:
+        db1 = db1.to(dbias_dtype)
+    return ShardedStep(o, lse, dq, dk, dv, db1, db2)
+
+
+def reduce_partials_cpu(partials, group=None) -> torch.Tensor:
+    """Host-side form of the dBias2 reduction used by the gloo tests: sum the
+    fp32 partial of every rank (same op the NCCL path issues)."""
+    t = partials.clone()
+    if dist.is_initialized() and dist.get_world_size(group) > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.SUM, group=group)
+    return t

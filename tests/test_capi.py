@@ -1,0 +1,78 @@
+"""The C-ABI library loads and exports every symbol include/evoattn.h declares;
+validation paths map to the reference error taxonomy (CPU only: no kernel runs)."""
+import ctypes as C
+import math
+import os
+import re
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _declared():
+    src = open(os.path.join(ROOT, "include", "evoattn.h")).read()
+    return sorted(set(re.findall(r"\b(evo_attn_\w+)\s*\(", src)))
+
+
+def test_header_declares_the_boundary():
+    names = _declared()
+    for must in ("evo_attn_fwd", "evo_attn_bwd", "evo_attn_fwd_workspace_size",
+                 "evo_attn_bwd_workspace_size", "evo_attn_last_error"):
+        assert must in names
+
+
+def test_library_exports_every_declared_symbol():
+    from paper_2310_04610_b200 import _native as N
+
+    lib = N.load()
+    for name in _declared():
+        assert hasattr(lib, name), name
+    assert set(N.EXPORTED) == set(_declared())
+    assert lib.evo_attn_version().decode().startswith("evoattn")
+
+
+def _desc(**kw):
+    from paper_2310_04610_b200 import _native as N
+
+    d = dict(Bo=1, N=4, L=64, H=2, D=32, dtype=N.EVO_BF16, scale=1 / math.sqrt(32), has_bias1=1,
+             has_bias2=1, dbias_dtype=N.EVO_F32, path=N.EVO_PATH_AUTO)
+    d.update(kw)
+    return N.Desc(**d)
+
+
+def test_workspace_sizes():
+    from paper_2310_04610_b200 import _native as N
+
+    lib = N.load()
+    d = _desc()
+    ws = lib.evo_attn_bwd_workspace_size(d)
+    # delta (B*H*L f32) + dbias2 fp32 (H*L*L) + dbias1 (B*L) at least
+    assert ws >= 4 * (4 * 2 * 64 + 2 * 64 * 64 + 4 * 64)
+    assert lib.evo_attn_bwd_workspace_size(_desc(L=0)) == 0
+
+
+def test_status_codes_without_gpu():
+    from paper_2310_04610_b200 import _native as N
+
+    lib = N.load()
+    st = lib.evo_attn_fwd(None, 1, 1, 1, None, None, 1, 1, None, 0, None)
+    assert st == N.EVO_ERR_USAGE
+    st = lib.evo_attn_fwd(_desc(L=0), 1, 1, 1, 1, 1, 1, 1, None, 0, None)
+    assert st == N.EVO_ERR_VALIDATION and "extents" in lib.evo_attn_last_error().decode()
+    st = lib.evo_attn_fwd(_desc(scale=float("inf")), 1, 1, 1, 1, 1, 1, 1, None, 0, None)
+    assert st == N.EVO_ERR_NUMERIC
+    st = lib.evo_attn_fwd(_desc(), 1, 1, 1, None, 1, 1, 1, None, 0, None)  # bias1 missing
+    assert st == N.EVO_ERR_VALIDATION
+    with pytest.raises(N.ValidationError):
+        N.check(N.EVO_ERR_VALIDATION)
+    st = lib.evo_attn_bwd(_desc(dbias_dtype=N.EVO_BF16), 1, 1, 1, 1, 1, 1, 1, 1, 1, 1, 1, None, 1,
+                          1, 1, 10**9, None)
+    assert st == N.EVO_ERR_VALIDATION  # accumulate requires fp32 dbias
+
+
+def test_simt_path_for_fp32():
+    from paper_2310_04610_b200 import _native as N
+
+    lib = N.load()
+    assert lib.evo_attn_resolved_path(_desc(dtype=N.EVO_F32, dbias_dtype=N.EVO_F32)) == N.EVO_PATH_SIMT

@@ -1,0 +1,126 @@
+"""GPU parity: the CUDA path (through the C-ABI) vs the oracle on identical inputs.
+
+Bar (north star): fp32 within 1e-4, bf16/f16 within 1e-2 of the F32 oracle on
+identically rounded inputs, normalized max-abs error, for O and all four
+gradients (dQ, dK, dV, dBias2), plus LSE and dBias1.
+"""
+import numpy as np
+import pytest
+import torch
+
+from tests.util import TOL, make_inputs, nmax_err, oracle_fwd_bwd, ref_rel_err
+
+pytestmark = pytest.mark.gpu
+
+TD = {"f32": torch.float32, "bf16": torch.bfloat16, "f16": torch.float16}
+
+
+def run_gpu(q, k, v, do, b1, b2, dtype, path="auto", need_dbias1=False, dbias_dtype=torch.float32):
+    import paper_2310_04610_b200 as E
+
+    t = lambda a: None if a is None else torch.tensor(a, dtype=TD[dtype], device="cuda")
+    tq, tk, tv, tdo, tb1, tb2 = map(t, (q, k, v, do, b1, b2))
+    o, lse = E.evoformer_attention_forward(tq, tk, tv, tb1, tb2, path=path)
+    dq, dk, dv, db1, db2 = E.evoformer_attention_backward(
+        tdo, tq, tk, tv, o, lse, tb1, tb2, need_dbias1=need_dbias1, dbias_dtype=dbias_dtype, path=path)
+    torch.cuda.synchronize()
+    n = lambda a: None if a is None else a.float().cpu().numpy()
+    return tuple(map(n, (o, lse, dq, dk, dv, db1, db2)))
+
+
+def check(shape, dtype, bias1=True, bias2=True, path="auto", need_dbias1=False, seed=0,
+          dbias_dtype=torch.float32, tol=None):
+    q, k, v, do, b1, b2 = make_inputs(*shape, dtype=dtype, bias1=bias1, bias2=bias2, seed=seed)
+    got = run_gpu(q, k, v, do, b1, b2, dtype, path, need_dbias1, dbias_dtype)
+    want = oracle_fwd_bwd(q, k, v, do, b1, b2, need_dbias1=need_dbias1)
+    tol = tol or TOL[dtype]
+    names = ["O", "LSE", "dQ", "dK", "dV", "dBias1", "dBias2"]
+    report = {}
+    for name, g, w in zip(names, got, want):
+        if w is None:
+            assert g is None or name == "dBias1", name
+            continue
+        assert g is not None, f"{name} missing"
+        assert np.isfinite(g).all(), f"{name} has non-finite values"
+        report[name] = (nmax_err(g, w), ref_rel_err(g, w))
+    bad = {k_: v_ for k_, v_ in report.items() if v_[0] > tol}
+    assert not bad, f"parity failed (tol {tol}): {bad}; all: {report}"
+    return report
+
+
+def test_config1_fp32_msa_row_mask_pair():
+    # BASELINE configs[0]: B=1 N_seq=32 N_res=64 H=8 D=32 fp32, mask + pair bias
+    check((1, 32, 64, 8, 32), "f32")
+
+
+def test_bf16_edge_tiles_l130():
+    # 130 exercises clipped edge tiles (attention_tiled.cpp:89,109; run.cpp:147)
+    check((1, 4, 130, 2, 32), "bf16")
+
+
+def test_bf16_no_bias_msa_col():
+    check((1, 6, 96, 2, 32), "bf16", bias1=False, bias2=False)
+
+
+def test_bf16_pair_bias_only_triangle():
+    check((1, 48, 48, 4, 32), "bf16", bias1=False)
+
+
+def test_bf16_outer_batch():
+    check((2, 3, 72, 2, 32), "bf16")
+
+
+def test_f16():
+    check((1, 4, 100, 2, 32), "f16")
+
+
+@pytest.mark.parametrize("D", [4, 8, 16, 64])
+def test_head_dims(D):
+    check((1, 3, 70, 2, D), "bf16")
+
+
+def test_fp32_small_d_reference_bench_shape():
+    # the reference's attn-bench default (4,130,2,8) F32 (run.cpp:137-157)
+    check((1, 4, 130, 2, 8), "f32")
+
+
+def test_dbias1_and_bf16_dbias_output():
+    check((1, 5, 64, 2, 32), "bf16", need_dbias1=True)
+    check((1, 5, 64, 2, 32), "bf16", need_dbias1=True, dbias_dtype=torch.bfloat16, tol=1.5e-2)
+
+
+def test_single_key_identity():
+    # L=1 => O = V
+    import paper_2310_04610_b200 as E
+
+    q, k, v, *_ = make_inputs(1, 4, 1, 2, 32, dtype="bf16", bias1=False, bias2=False)
+    tv = torch.tensor(v, dtype=torch.bfloat16, device="cuda")
+    o, _ = E.evoformer_attention_forward(torch.tensor(q, dtype=torch.bfloat16, device="cuda"),
+                                         torch.tensor(k, dtype=torch.bfloat16, device="cuda"), tv)
+    assert torch.equal(o, tv)
+
+
+@pytest.mark.parametrize("path", ["simt", "auto"])
+def test_paths_agree(path):
+    check((1, 2, 128, 2, 32), "bf16", path=path)
+
+
+def test_launches_counted():
+    import paper_2310_04610_b200 as E
+
+    q, k, v, do, b1, b2 = make_inputs(1, 2, 64, 2, 32)
+    t = lambda a: torch.tensor(a, dtype=torch.bfloat16, device="cuda")
+    o, lse = E.evoformer_attention_forward(t(q), t(k), t(v), t(b1), t(b2))
+    assert E.last_launch_count() >= 1
+
+
+def test_validation_errors_map_to_taxonomy():
+    import paper_2310_04610_b200 as E
+
+    q = torch.zeros(1, 2, 8, 2, 32, dtype=torch.bfloat16, device="cuda")
+    with pytest.raises(E.ValidationError):
+        E.evoformer_attention_forward(q, q, q[..., :16].contiguous())
+    with pytest.raises(E.ValidationError):
+        E.evoformer_attention_forward(q, q, q, bias2=torch.zeros(1, 1, 2, 8, 7, dtype=torch.bfloat16, device="cuda"))
+    with pytest.raises(E.NumericError):
+        E.evoformer_attention_forward(q, q, q, scale=float("nan"))
