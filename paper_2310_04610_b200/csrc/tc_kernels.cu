@@ -1,24 +1,181 @@
-// tc_kernels.cu — tcgen05 kernels (placeholder until the TMEM/TMA kernels land).
+// tc_kernels.cu — host side of the tcgen05 kernels: TMA tensor maps, shared-memory
+// budgets, persistent grid sizing (one CTA per SM) and launches.
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
+#include <cstdio>
+#include <mutex>
+
+#include "tc_fwd.cuh"
 #include "tc_kernels.cuh"
 
 namespace evo {
 namespace tc {
 
-bool device_supported() { return false; }
+namespace {
+
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = (PFN_cuTensorMapEncodeTiled_v12000)p;
+  });
+  return fn;
+}
+
+int sm_count() {
+  int dev = 0, n = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+  return n;
+}
+
+CUtensorMapSwizzle swz(int row_bytes) {
+  return row_bytes == 128 ? CU_TENSOR_MAP_SWIZZLE_128B
+         : row_bytes == 64 ? CU_TENSOR_MAP_SWIZZLE_64B
+                           : CU_TENSOR_MAP_SWIZZLE_32B;
+}
+
+// (B, L, H, D) row-major as a 4-D map (D, H, L, B); box (D, 1, rows, 1).
+bool map_bl_hd(CUtensorMap* m, const void* base, const Shape& s, int rows, CUtensorMapDataType dt,
+               int esize, std::string* err) {
+  cuuint64_t dims[4] = {(cuuint64_t)s.D, (cuuint64_t)s.H, (cuuint64_t)s.L, (cuuint64_t)s.B};
+  cuuint64_t strides[3] = {(cuuint64_t)s.D * esize, (cuuint64_t)s.H * s.D * esize,
+                           (cuuint64_t)s.L * s.H * s.D * esize};
+  cuuint32_t box[4] = {(cuuint32_t)s.D, 1, (cuuint32_t)rows, 1};
+  cuuint32_t es[4] = {1, 1, 1, 1};
+  CUresult r = encode_fn()(m, dt, 4, const_cast<void*>(base), dims, strides, box, es,
+                           CU_TENSOR_MAP_INTERLEAVE_NONE, swz(s.D * esize), CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                           CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) {
+    *err = "cuTensorMapEncodeTiled (B,L,H,D) failed: " + std::to_string((int)r);
+    return false;
+  }
+  return true;
+}
+
+// bias2 [Bo*H, L, L] as 3-D (Lj, Li, plane); box (64, 128, 1), 128B swizzle.
+bool map_bias(CUtensorMap* m, const void* base, const Shape& s, int Bo, CUtensorMapDataType dt,
+              std::string* err) {
+  cuuint64_t dims[3] = {(cuuint64_t)s.L, (cuuint64_t)s.L, (cuuint64_t)Bo * s.H};
+  cuuint64_t strides[2] = {(cuuint64_t)s.L * 2, (cuuint64_t)s.L * s.L * 2};
+  cuuint32_t box[3] = {64, 128, 1};
+  cuuint32_t es[3] = {1, 1, 1};
+  CUresult r = encode_fn()(m, dt, 3, const_cast<void*>(base), dims, strides, box, es,
+                           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                           CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) {
+    *err = "cuTensorMapEncodeTiled (bias2) failed: " + std::to_string((int)r);
+    return false;
+  }
+  return true;
+}
+
+template <int D>
+size_t fwd_smem_bytes(int nbias_slots, int nKT) {
+  using S = FwdSmem<D>;
+  size_t b = 1024;  // alignment slack
+  b += 2 * S::kTileBytes + 2 * S::kStages * S::kTileBytes;
+  b += (size_t)nbias_slots * S::kBiasTileBytes;
+  b += (size_t)nKT * kBN * 4;
+  b += (4 + 2 * S::kStages + 10 + 2 * nbias_slots) * 8 + 16;
+  return b;
+}
+
+constexpr size_t kMaxSmem = 227 * 1024;
+
+template <int D, bool F16>
+evo_status launch_fwd(const evo_attn_desc* d, const Shape& s, const void* q, const void* k, const void* v,
+                      void* o, float* lse, cudaStream_t st, int* launches, std::string* err) {
+  const CUtensorMapDataType dt = F16 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT16 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16;
+  CUtensorMap tq, tk, tv, tb;
+  memset(&tb, 0, sizeof(tb));
+  if (!map_bl_hd(&tq, q, s, kBM, dt, 2, err) || !map_bl_hd(&tk, k, s, kBN, dt, 2, err) ||
+      !map_bl_hd(&tv, v, s, kBN, dt, 2, err))
+    return EVO_ERR_CUDA;
+  FwdParams p{};
+  p.B = s.B; p.N = s.N; p.L = s.L; p.H = s.H; p.Bo = (int)d->Bo;
+  p.nQT = (s.L + kBM - 1) / kBM;
+  p.nKT = (s.L + kBN - 1) / kBN;
+  p.total = (long long)p.Bo * p.H * p.nQT * p.N;
+  p.scale_log2 = s.scale_log2;
+  p.bias1 = s.bias1;
+  p.bias2 = s.bias2;
+  p.o = o;
+  p.lse = lse;
+  p.bias_mode = kBiasNone;
+  p.nbias_slots = 0;
+  if (s.bias2) {
+    if (s.L % 8 != 0) {
+      p.bias_mode = kBiasGlobal;
+    } else {
+      if (!map_bias(&tb, s.bias2, s, p.Bo, dt, err)) return EVO_ERR_CUDA;
+      if (fwd_smem_bytes<D>(p.nKT, p.nKT) <= kMaxSmem) {
+        p.bias_mode = kBiasResident;
+        p.nbias_slots = p.nKT;
+      } else {
+        p.bias_mode = kBiasStreamed;
+        p.nbias_slots = 2;
+      }
+    }
+  }
+  const size_t smem = fwd_smem_bytes<D>(p.nbias_slots, p.nKT);
+  if (smem > kMaxSmem) {
+    *err = "forward shared-memory budget exceeded (L too large)";
+    return EVO_ERR_UNSUPPORTED;
+  }
+  auto kern = fwd_kernel<D, F16>;
+  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  const long long grid = std::min<long long>(p.total, sm_count());
+  kern<<<(unsigned)grid, kFwdThreads, smem, st>>>(tq, tk, tv, tb, p);
+  ++*launches;
+  return EVO_OK;
+}
+
+}  // namespace
+
+bool device_supported() {
+  static int ok = -1;
+  if (ok < 0) {
+    int dev = 0, major = 0, minor = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) {
+      cudaGetLastError();
+      return false;
+    }
+    cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev);
+    cudaDeviceGetAttribute(&minor, cudaDevAttrComputeCapabilityMinor, dev);
+    ok = (major == 10 && minor == 0 && encode_fn() != nullptr) ? 1 : 0;
+  }
+  return ok == 1;
+}
+
 size_t fwd_scratch_bytes(const evo_attn_desc*) { return 0; }
 size_t bwd_scratch_bytes(const evo_attn_desc*) { return 0; }
+bool bwd_available(const evo_attn_desc*) { return false; }
 
-evo_status fwd(const evo_attn_desc*, const Shape&, const void*, const void*, const void*, void*,
-               float*, void*, cudaStream_t, int*, std::string* err) {
-  *err = "tcgen05 forward not built";
+evo_status bwd(const evo_attn_desc*, const Shape&, const void*, const void*, const void*, const void*,
+               const float*, const float*, void*, void*, void*, float*, float*, void*, cudaStream_t, int*,
+               std::string* err) {
+  *err = "tcgen05 backward not built";
   return EVO_ERR_UNSUPPORTED;
 }
 
-evo_status bwd(const evo_attn_desc*, const Shape&, const void*, const void*, const void*,
-               const void*, const float*, const float*, void*, void*, void*, float*, float*,
-               void*, cudaStream_t, int*, std::string* err) {
-  *err = "tcgen05 backward not built";
-  return EVO_ERR_UNSUPPORTED;
+evo_status fwd(const evo_attn_desc* d, const Shape& s, const void* q, const void* k, const void* v, void* o,
+               float* lse, void*, cudaStream_t st, int* launches, std::string* err) {
+  const bool f16 = d->dtype == EVO_F16;
+  switch (d->D) {
+    case 16: return f16 ? launch_fwd<16, true>(d, s, q, k, v, o, lse, st, launches, err)
+                        : launch_fwd<16, false>(d, s, q, k, v, o, lse, st, launches, err);
+    case 32: return f16 ? launch_fwd<32, true>(d, s, q, k, v, o, lse, st, launches, err)
+                        : launch_fwd<32, false>(d, s, q, k, v, o, lse, st, launches, err);
+    case 64: return f16 ? launch_fwd<64, true>(d, s, q, k, v, o, lse, st, launches, err)
+                        : launch_fwd<64, false>(d, s, q, k, v, o, lse, st, launches, err);
+    default: *err = "tcgen05 forward supports D in {16, 32, 64}"; return EVO_ERR_UNSUPPORTED;
+  }
 }
 
 }  // namespace tc

@@ -10,6 +10,7 @@ namespace tc {
 bool device_supported();
 size_t fwd_scratch_bytes(const evo_attn_desc* d);
 size_t bwd_scratch_bytes(const evo_attn_desc* d);
+bool bwd_available(const evo_attn_desc* d);
 
 evo_status fwd(const evo_attn_desc* d, const Shape& s, const void* q, const void* k, const void* v,
                void* o, float* lse, void* workspace, cudaStream_t st, int* launches,

@@ -21,7 +21,8 @@ def make_inputs(Bo, Nr, L, H, D, dtype="bf16", bias1=True, bias2=True, seed=0, m
     if bias1:
         m = rng.uniform(0, 1, (Bo, Nr, 1, 1, L)) < mask_rate
         m[..., 0] = False
-        b1 = np.where(m, np.float32(-1e9), np.float32(0)).astype(np.float32)
+        neg = -3.0e4 if dtype == "f16" else -1e9  # -1e9 overflows fp16
+        b1 = np.where(m, np.float32(neg), np.float32(0)).astype(np.float32)
     rnd = (lambda a: a) if dtype == "f32" else (lambda a: None if a is None else O.round_to(a, dtype).astype(np.float32))
     return tuple(None if a is None else rnd(a) for a in (q, k, v, do, b1, b2))
 
