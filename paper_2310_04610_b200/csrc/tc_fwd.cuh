@@ -4,18 +4,24 @@
 // (S = scale*QK^T + bias, online softmax over key tiles, O = acc/l, LSE = m + ln l), plus the
 // DS4Sci mask bias1[b, j]. Layout and schedule are B200-first:
 //
-//  * persistent CTAs (one per SM) walk a contiguous range of (ob, h, q-tile, row) work items,
-//    rows innermost, so one CTA keeps the pair-bias row block bias2[ob, h, q-tile, :] resident in
-//    shared memory (TMA, 128B swizzle) and reuses it for every MSA row it processes — the bias is
-//    read from L2 once per CTA instead of once per row (the paper's on-the-fly broadcast).
-//  * warp 0: TMA producer (Q per row, K/V per key tile through a 3-stage ring).
-//    warp 1: single-thread tcgen05.mma issuer: S = Q K^T (SS, K-major) into a double-buffered
-//            128x128 fp32 TMEM tile; O_j = P_j V_j (TS: P read from TMEM, V MN-major) into a
-//            double-buffered 128xD fp32 TMEM tile.
-//    warps 2-5: softmax warpgroup, one thread per query row (TMEM lane): S -> registers,
-//            bias1/bias2 add, online max/sum in the log2 domain (ex2.approx), P (bf16) written
-//            back into the S columns (FA4-style aliasing), per-tile O_j folded into a register
-//            accumulator with the running rescale factor; epilogue writes O and LSE.
+//  * Persistent CTAs walk work items (ob, h, q-tile, row) with rows innermost. A run of items with
+//    the same (ob, h, q-tile) is a "segment": its pair-bias row block bias2[ob, h, q-tile rows, :]
+//    is loaded into shared memory once by TMA (128B swizzle, one 16 KB box per 64 keys) and
+//    reused for every MSA row of the segment — the paper's on-the-fly broadcast, read from L2
+//    once per CTA instead of once per row. L too long for residency: bias tiles stream per key
+//    tile and are shared by the rows in flight. When the grid splits evenly, CTAs get aligned
+//    row ranges so the q-tiles of one (row, head) run concurrently and share K/V through L2.
+//  * warp 0: TMA producer. warp 1: single-thread tcgen05.mma issuer.
+//    NWG independent softmax warpgroups (3 for D <= 32), each owning whole MSA rows: rows of a
+//    segment are dealt round-robin, so warpgroups sit at different phases (bias math, MUFU, TMEM
+//    traffic) and overlap instead of contending. Per warpgroup: a double-buffered 128x64 fp32 S
+//    tile in TMEM (S = Q K^T, SS-MMA) -> registers (one thread = one query row = one TMEM lane),
+//    bias1 + bias2 add and online max/sum in the log2 domain with packed f32x2 math, P (bf16)
+//    written back over S and consumed by a K=64 TS-MMA that accumulates O in TMEM. The running max
+//    only moves (rescaling O in TMEM) when it grows by more than 2^8 (FA4's lazy rescale), so the
+//    steady state has no per-tile O traffic; O is read once per row.
+//  * TMEM per warpgroup w: S buffers [W*w, W*w+64) [W*w+64, W*w+128), O [W*w+128, W*w+128+D),
+//    W = 128 + D.
 #pragma once
 #include "common.cuh"
 #include "tc_ptx.cuh"
@@ -23,42 +29,44 @@
 namespace evo {
 namespace tc {
 
-constexpr int kBM = 128;   // query rows per tile (UMMA M, TMEM lanes)
-constexpr int kBN = 128;   // keys per tile (UMMA N of S)
-constexpr int kFwdThreads = 192;
+constexpr int kBM = 128;                 // query rows per tile (UMMA M, TMEM lanes)
+constexpr int kBN = 64;                  // keys per tile (UMMA N of S)
+constexpr float kRescaleThreshold = 8.f;  // log2 units
 
-// bias2 delivery
+template <int D>
+struct FwdCfg {
+  static constexpr int NWG = D <= 32 ? 3 : 2;          // softmax warpgroups
+  static constexpr int kThreads = 64 + 128 * NWG;
+  static constexpr int kRowBytes = D * 2;
+  static constexpr int kTileQ = kBM * kRowBytes;       // Q tile
+  static constexpr int kTileKV = kBN * kRowBytes;      // K or V tile
+  static constexpr int kStages = 2 * NWG;              // K/V ring depth
+  static constexpr int kBiasTile = kBM * kBN * 2;      // 16 KB
+  static constexpr int kWGcols = 128 + D;              // TMEM columns per warpgroup
+};
+
 enum BiasMode : int { kBiasNone = 0, kBiasResident = 1, kBiasStreamed = 2, kBiasGlobal = 3 };
 
 struct FwdParams {
   int B, N, L, H, Bo;
   int nQT, nKT;
   long long total;   // work items = Bo*H*nQT*N
+  int aligned;       // 1: CTA c owns part c%split of unit c/split; 0: flat contiguous split
+  int split;
   float scale_log2;
   int bias_mode;
-  int nbias_slots;   // resident: nKT; streamed: 2
+  int nbias_slots;   // resident: nKT; streamed: 3
+  int b1_tma;        // bias1 rows fetched by TMA bulk copy (L % 8 == 0)
   const void* bias1;  // [B, L] or null
-  const void* bias2;  // [Bo, H, L, L] (used directly in kBiasGlobal mode)
+  const void* bias2;  // [Bo, H, L, L] (read directly in kBiasGlobal mode)
   void* o;           // [B, L, H, D]
   float* lse;        // [B, H, L]
+  unsigned long long* trace;  // bring-up timeline of CTA 0 (null in production)
 };
 
-template <int D>
-struct FwdSmem {
-  static constexpr int kRowBytes = D * 2;
-  static constexpr int kTileBytes = kBM * kRowBytes;      // Q/K/V tile
-  static constexpr int kStages = D == 64 ? 2 : 3;
-  static constexpr int kBiasTileBytes = kBM * kBN * 2;    // 32 KB
-};
-
-__device__ __forceinline__ void decode_item(long long t, int N, int nQT, int H, int& ob, int& h, int& qt,
-                                            int& n) {
-  n = (int)(t % N);
-  long long u = t / N;
-  qt = (int)(u % nQT);
-  u /= nQT;
-  h = (int)(u % H);
-  ob = (int)(u / H);
+enum TraceEv { kTrKV = 0, kTrS = 1, kTrSseen = 2, kTrP0 = 3, kTrP1 = 4, kTrPV = 5, kTrRowEnd = 6, kTrRowStart = 7 };
+__device__ __forceinline__ void trace(const FwdParams& p, int ev, uint32_t tile) {
+  if (p.trace && blockIdx.x == 0 && tile < 64) p.trace[ev * 64 + tile] = clock64();
 }
 
 template <bool F16>
@@ -66,53 +74,102 @@ __device__ __forceinline__ float load_half(const void* base, size_t idx) {
   const unsigned short u = ((const unsigned short*)base)[idx];
   return F16 ? __half2float(__ushort_as_half(u)) : __uint_as_float((uint32_t)u << 16);
 }
+template <bool F16>
+__device__ __forceinline__ float2 unpack2(uint32_t w) {  // two packed 16-bit floats, low first
+  if constexpr (F16) {
+    __half2 hh = *reinterpret_cast<__half2*>(&w);
+    return __half22float2(hh);
+  } else {
+    return make_float2(__uint_as_float(w << 16), __uint_as_float(w & 0xFFFF0000u));
+  }
+}
+__device__ __forceinline__ uint4 lds128(uint32_t a) {
+  uint4 v;
+  asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   ptx::smem_u32(dst)),
+               "l"(src), "r"(bytes), "r"(ptx::smem_u32(bar))
+               : "memory");
+}
 
-template <int D, bool F16>
-__global__ void __launch_bounds__(kFwdThreads, 1)
+// One CTA's item range, cut into segments at (ob, h, q-tile) boundaries. Inside a segment the
+// rows go out in groups of NWG (row s0 + g*NWG + w -> warpgroup w).
+struct Walker {
+  long long t0, t1, N;
+  __device__ long long seg_end(long long s) const {
+    const long long e = (s / N + 1) * N;
+    return e < t1 ? e : t1;
+  }
+};
+__device__ __forceinline__ Walker make_walker(const FwdParams& p) {
+  if (p.aligned) {
+    const long long unit = blockIdx.x / p.split, part = blockIdx.x % p.split;
+    const long long base = unit * p.N;
+    return Walker{base + p.N * part / p.split, base + p.N * (part + 1) / p.split, p.N};
+  }
+  return Walker{p.total * blockIdx.x / gridDim.x, p.total * (blockIdx.x + 1) / gridDim.x, p.N};
+}
+struct SegInfo {
+  int ob, h, qt, n0;  // n0 = row index (within N) of the segment's first item
+};
+__device__ __forceinline__ SegInfo seg_info(long long s0, const FwdParams& p) {
+  SegInfo si;
+  long long u = s0 / p.N;
+  si.n0 = (int)(s0 - u * p.N);
+  si.qt = (int)(u % p.nQT);
+  u /= p.nQT;
+  si.h = (int)(u % p.H);
+  si.ob = (int)(u / p.H);
+  return si;
+}
+
+template <int D, bool F16, int BM>
+__global__ void __launch_bounds__(FwdCfg<D>::kThreads, 1)
     fwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
                const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmB2,
                const FwdParams p) {
-  using S = FwdSmem<D>;
+  using C = FwdCfg<D>;
+  constexpr int NWG = C::NWG;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
-  uint8_t* sQ = smem;                                        // 2 x tile
-  uint8_t* sK = sQ + 2 * S::kTileBytes;                      // stages x tile
-  uint8_t* sV = sK + S::kStages * S::kTileBytes;             // stages x tile
-  uint8_t* sBias = sV + S::kStages * S::kTileBytes;          // nbias_slots x 32 KB
-  float* sB1 = (float*)(sBias + (size_t)p.nbias_slots * S::kBiasTileBytes);  // nKT*128 floats
-  uint64_t* bars = (uint64_t*)(sB1 + p.nKT * kBN);
-  uint64_t* q_full = bars;                 // 2
-  uint64_t* q_empty = bars + 2;            // 2
-  uint64_t* kv_full = bars + 4;            // stages
-  uint64_t* kv_empty = kv_full + S::kStages;
-  uint64_t* s_full = kv_empty + S::kStages;  // 2
-  uint64_t* s_free = s_full + 2;             // 2
-  uint64_t* p_full = s_free + 2;             // 2
-  uint64_t* o_full = p_full + 2;             // 2
-  uint64_t* o_free = o_full + 2;             // 2
-  uint64_t* bias_full = o_free + 2;          // nbias_slots
+  const int LP = p.nKT * kBN;                               // padded key count
+  uint8_t* sQ = smem;                                       // [NWG][2] Q tiles
+  uint8_t* sK = sQ + NWG * 2 * C::kTileQ;                   // [stages]
+  uint8_t* sV = sK + C::kStages * C::kTileKV;               // [stages]
+  uint8_t* sBias = sV + C::kStages * C::kTileKV;            // [nbias_slots] x 16 KB
+  uint16_t* sB1raw = (uint16_t*)(sBias + (size_t)p.nbias_slots * C::kBiasTile);  // [NWG][2][LP] bf16
+  float* sB1 = (float*)(sB1raw + NWG * 2 * LP);              // [NWG][2][LP] fp32 * log2e
+  uint64_t* bars = (uint64_t*)(sB1 + NWG * 2 * LP);
+  uint64_t* q_full = bars;                       // [NWG][2] Q (+ bias1 row) landed
+  uint64_t* q_empty = q_full + 2 * NWG;          // [NWG][2] MMA commit + the warpgroup
+  uint64_t* s_full = q_empty + 2 * NWG;          // [NWG][2]
+  uint64_t* s_free = s_full + 2 * NWG;           // [NWG][2] PV reading that buffer done
+  uint64_t* p_full = s_free + 2 * NWG;           // [NWG][2]
+  uint64_t* o_free = p_full + 2 * NWG;           // [NWG] O read out at row end
+  uint64_t* kv_full = o_free + NWG;              // [stages]
+  uint64_t* kv_empty = kv_full + C::kStages;     // [stages]
+  uint64_t* bias_full = kv_empty + C::kStages;   // [nbias_slots]
   uint64_t* bias_empty = bias_full + p.nbias_slots;
   uint32_t* tmem_slot = (uint32_t*)(bias_empty + p.nbias_slots);
 
   const int warp = threadIdx.x / 32;
   const int lane = threadIdx.x % 32;
-
-  // contiguous slice of the work list for this CTA
-  const long long t0 = p.total * blockIdx.x / gridDim.x;
-  const long long t1 = p.total * (blockIdx.x + 1) / gridDim.x;
+  const Walker W = make_walker(p);
 
   if (threadIdx.x == 0) {
-    ptx::mbar_init(&q_full[0], 1); ptx::mbar_init(&q_full[1], 1);
-    ptx::mbar_init(&q_empty[0], 1); ptx::mbar_init(&q_empty[1], 1);
-    for (int s = 0; s < S::kStages; ++s) { ptx::mbar_init(&kv_full[s], 1); ptx::mbar_init(&kv_empty[s], 1); }
-    for (int s = 0; s < 2; ++s) {
+    for (int s = 0; s < 2 * NWG; ++s) {
+      ptx::mbar_init(&q_full[s], 1);
+      ptx::mbar_init(&q_empty[s], 2);
       ptx::mbar_init(&s_full[s], 1);
       ptx::mbar_init(&s_free[s], 1);
       ptx::mbar_init(&p_full[s], 128);
-      ptx::mbar_init(&o_full[s], 1);
-      ptx::mbar_init(&o_free[s], 128);
     }
-    for (int s = 0; s < p.nbias_slots; ++s) { ptx::mbar_init(&bias_full[s], 1); ptx::mbar_init(&bias_empty[s], 128); }
+    for (int w = 0; w < NWG; ++w) ptx::mbar_init(&o_free[w], 128);
+    for (int s = 0; s < C::kStages; ++s) { ptx::mbar_init(&kv_full[s], 1); ptx::mbar_init(&kv_empty[s], 1); }
+    for (int s = 0; s < p.nbias_slots; ++s) { ptx::mbar_init(&bias_full[s], 1); ptx::mbar_init(&bias_empty[s], NWG); }
     ptx::fence_barrier_init();
   }
   if (warp == 1) ptx::tmem_alloc(tmem_slot, 512);
@@ -121,269 +178,373 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
   ptx::tc_fence_after();
   const uint32_t tmem = *tmem_slot;
 
-  const uint32_t idS = ptx::instr_desc(kBM, kBN, F16, false, false);
-  const uint32_t idO = ptx::instr_desc(kBM, D, F16, false, true);
-  constexpr uint32_t kSw = ptx::swizzle_code(S::kRowBytes);
-  const bool streamed = p.bias_mode == kBiasStreamed;
-  const bool resident = p.bias_mode == kBiasResident;
+  constexpr uint32_t kSw = ptx::swizzle_code(C::kRowBytes);
+  constexpr bool streamed = BM == kBiasStreamed;
+  constexpr bool resident = BM == kBiasResident;
 
   if (warp == 0) {
-    // ===================================================== TMA producer
     if (lane == 0) {
+      // ===================================================== TMA producer
       ptx::tma_prefetch(&tmQ); ptx::tma_prefetch(&tmK); ptx::tma_prefetch(&tmV);
       if (resident || streamed) ptx::tma_prefetch(&tmB2);
-      int qs = 0; uint32_t qph = 0;
+      uint32_t qc[NWG];  // Q loads per warpgroup: slot = qc & 1, use parity = (qc >> 1) & 1
+#pragma unroll
+      for (int w = 0; w < NWG; ++w) qc[w] = 0;
       int ks = 0; uint32_t kph = 0;
       int bslot = 0; uint32_t bph = 0;
-      long long cur_unit = -1;
-      for (long long t = t0; t < t1; ++t) {
-        int ob, h, qt, n;
-        decode_item(t, p.N, p.nQT, p.H, ob, h, qt, n);
-        const int b = ob * p.N + n;
-        const long long unit = t / p.N;
-        if (resident && unit != cur_unit) {
-          cur_unit = unit;
+      const uint32_t b1_bytes = (uint32_t)p.L * 2;
+      const bool b1t = p.bias1 && p.b1_tma;
+      for (long long s0 = W.t0; s0 < W.t1; s0 = W.seg_end(s0)) {
+        const long long s1 = W.seg_end(s0);
+        const SegInfo si = seg_info(s0, p);
+        const int plane = si.ob * p.H + si.h;
+        if (resident) {
           for (int j = 0; j < p.nKT; ++j) {
             ptx::mbar_wait(&bias_empty[j], bph ^ 1);
-            ptx::mbar_expect_tx(&bias_full[j], S::kBiasTileBytes);
-            uint8_t* dst = sBias + (size_t)j * S::kBiasTileBytes;
-            ptx::tma_load_3d(dst, &tmB2, &bias_full[j], j * kBN, qt * kBM, ob * p.H + h);
-            ptx::tma_load_3d(dst + 16384, &tmB2, &bias_full[j], j * kBN + 64, qt * kBM, ob * p.H + h);
+            ptx::mbar_expect_tx(&bias_full[j], C::kBiasTile);
+            ptx::tma_load_3d(sBias + (size_t)j * C::kBiasTile, &tmB2, &bias_full[j], j * kBN, si.qt * kBM, plane);
           }
           bph ^= 1;
         }
-        ptx::mbar_wait(&q_empty[qs], qph ^ 1);
-        ptx::mbar_expect_tx(&q_full[qs], S::kTileBytes);
-        ptx::tma_load_4d(sQ + qs * S::kTileBytes, &tmQ, &q_full[qs], 0, h, qt * kBM, b);
-        if (++qs == 2) { qs = 0; qph ^= 1; }
-        for (int j = 0; j < p.nKT; ++j) {
-          ptx::mbar_wait(&kv_empty[ks], kph ^ 1);
-          ptx::mbar_expect_tx(&kv_full[ks], 2 * S::kTileBytes);
-          ptx::tma_load_4d(sK + ks * S::kTileBytes, &tmK, &kv_full[ks], 0, h, j * kBN, b);
-          ptx::tma_load_4d(sV + ks * S::kTileBytes, &tmV, &kv_full[ks], 0, h, j * kBN, b);
-          if (++ks == S::kStages) { ks = 0; kph ^= 1; }
-          if (streamed) {
-            ptx::mbar_wait(&bias_empty[bslot], bph ^ 1);
-            ptx::mbar_expect_tx(&bias_full[bslot], S::kBiasTileBytes);
-            uint8_t* dst = sBias + (size_t)bslot * S::kBiasTileBytes;
-            ptx::tma_load_3d(dst, &tmB2, &bias_full[bslot], j * kBN, qt * kBM, ob * p.H + h);
-            ptx::tma_load_3d(dst + 16384, &tmB2, &bias_full[bslot], j * kBN + 64, qt * kBM, ob * p.H + h);
-            if (++bslot == p.nbias_slots) { bslot = 0; bph ^= 1; }
+        int n = si.n0;
+        for (long long a = s0; a < s1; a += NWG, n += NWG) {
+          const int np = (int)min((long long)NWG, s1 - a);
+#pragma unroll
+          for (int w = 0; w < NWG; ++w) {
+            if (w >= np) break;
+            const int b = si.ob * p.N + n + w;
+            const uint32_t slot = qc[w] & 1, ph = (qc[w] >> 1) & 1;
+            ptx::mbar_wait(&q_empty[w * 2 + slot], ph ^ 1);
+            ptx::mbar_expect_tx(&q_full[w * 2 + slot], C::kTileQ + (b1t ? b1_bytes : 0));
+            ptx::tma_load_4d(sQ + (w * 2 + slot) * C::kTileQ, &tmQ, &q_full[w * 2 + slot], 0, si.h, si.qt * kBM, b);
+            if (b1t)
+              bulk_g2s(sB1raw + (w * 2 + slot) * LP, (const uint16_t*)p.bias1 + (size_t)b * p.L, b1_bytes,
+                       &q_full[w * 2 + slot]);
+            ++qc[w];
+          }
+          for (int j = 0; j < p.nKT; ++j) {
+            if (streamed) {
+              ptx::mbar_wait(&bias_empty[bslot], bph ^ 1);
+              ptx::mbar_expect_tx(&bias_full[bslot], C::kBiasTile);
+              ptx::tma_load_3d(sBias + (size_t)bslot * C::kBiasTile, &tmB2, &bias_full[bslot], j * kBN,
+                               si.qt * kBM, plane);
+              if (++bslot == p.nbias_slots) { bslot = 0; bph ^= 1; }
+            }
+#pragma unroll
+            for (int w = 0; w < NWG; ++w) {
+              if (w >= np) break;
+              const int b = si.ob * p.N + n + w;
+              ptx::mbar_wait(&kv_empty[ks], kph ^ 1);
+              ptx::mbar_expect_tx(&kv_full[ks], 2 * C::kTileKV);
+              ptx::tma_load_4d(sK + ks * C::kTileKV, &tmK, &kv_full[ks], 0, si.h, j * kBN, b);
+              ptx::tma_load_4d(sV + ks * C::kTileKV, &tmV, &kv_full[ks], 0, si.h, j * kBN, b);
+              if (++ks == C::kStages) { ks = 0; kph ^= 1; }
+            }
           }
         }
       }
     }
   } else if (warp == 1) {
-    // ===================================================== MMA issuer
     if (lane == 0) {
-      int qs = 0; uint32_t qph = 0;
+      // ===================================================== MMA issuer
+      const uint32_t idS = ptx::instr_desc(kBM, kBN, F16, false, false);
+      const uint32_t idO = ptx::instr_desc(kBM, D, F16, false, true);
+      uint32_t qc[NWG], tc[NWG], rc[NWG];  // per warpgroup: Q loads, tiles, rows
+#pragma unroll
+      for (int w = 0; w < NWG; ++w) qc[w] = tc[w] = rc[w] = 0;
       int ks = 0; uint32_t kph = 0;
-      long long tt = 0;  // global tile counter
-      bool pend = false; long long pt = 0; int pks = 0;
-      auto issue_pv = [&](long long tp, int ksp) {
-        const int sb = (int)(tp & 1);
-        const uint32_t ph = (uint32_t)((tp >> 1) & 1);
-        ptx::mbar_wait(&p_full[sb], ph);
-        ptx::mbar_wait(&o_free[sb], ph ^ 1);
-        ptx::tc_fence_after();
-        const uint32_t vbase = ptx::smem_u32(sV + ksp * S::kTileBytes);
+      // PVs of the previous key tile, issued after the next tile's S MMAs
+      int pn = 0;
+      int pks[NWG];
+      uint32_t ptc[NWG];
+      bool pfirst[NWG];
+      auto issue_pvs = [&]() {
 #pragma unroll
-        for (int kk = 0; kk < kBN / 16; ++kk) {
-          // V is MN-major: 16 keys = 2 x 8-row swizzle atoms, SBO = 8 rows
-          const uint64_t bd = ptx::smem_desc(vbase + kk * 16 * S::kRowBytes, 16 * S::kRowBytes,
-                                             8 * S::kRowBytes, kSw);
-          ptx::mma_ts(tmem + 256 + sb * D, tmem + sb * 128 + kk * 8, bd, idO, kk > 0);
-        }
-        ptx::tc_commit(&o_full[sb]);
-        ptx::tc_commit(&s_free[sb]);
-        ptx::tc_commit(&kv_empty[ksp]);
-      };
-      for (long long t = t0; t < t1; ++t) {
-        ptx::mbar_wait(&q_full[qs], qph);
-        const uint32_t qbase = ptx::smem_u32(sQ + qs * S::kTileBytes);
-        for (int j = 0; j < p.nKT; ++j) {
-          const int sb = (int)(tt & 1);
-          ptx::mbar_wait(&kv_full[ks], kph);
-          ptx::mbar_wait(&s_free[sb], (uint32_t)(((tt >> 1) & 1) ^ 1));
-          ptx::tc_fence_after();
-          const uint32_t kbase = ptx::smem_u32(sK + ks * S::kTileBytes);
-#pragma unroll
-          for (int kk = 0; kk < D / 16; ++kk) {
-            const uint64_t ad = ptx::smem_desc(qbase + kk * 32, 16, 8 * S::kRowBytes, kSw);
-            const uint64_t bd = ptx::smem_desc(kbase + kk * 32, 16, 8 * S::kRowBytes, kSw);
-            ptx::mma_ss(tmem + sb * 128, ad, bd, idS, kk > 0);
+        for (int w = 0; w < NWG; ++w) {
+          if (w >= pn) break;
+          const uint32_t sb = ptc[w] & 1;
+          ptx::mbar_wait_spin(&p_full[w * 2 + sb], (ptc[w] >> 1) & 1);
+          if (pfirst[w]) {  // first tile of a row overwrites O: the previous row must be read out
+            ptx::mbar_wait_spin(&o_free[w], (rc[w] & 1) ^ 1);
+            ++rc[w];
           }
-          ptx::tc_commit(&s_full[sb]);
-          if (j == p.nKT - 1) ptx::tc_commit(&q_empty[qs]);
-          if (pend) issue_pv(pt, pks);
-          pend = true; pt = tt; pks = ks;
-          if (++ks == S::kStages) { ks = 0; kph ^= 1; }
-          ++tt;
+          ptx::tc_fence_after();
+          const uint32_t vbase = ptx::smem_u32(sV + pks[w] * C::kTileKV);
+          const uint32_t wbase = tmem + w * C::kWGcols;
+#pragma unroll
+          for (int kk = 0; kk < kBN / 16; ++kk) {
+            // V is MN-major: 16 keys = two 8-row swizzle atoms (SBO = 8 rows)
+            const uint64_t bd = ptx::smem_desc(vbase + kk * 16 * C::kRowBytes, 16 * C::kRowBytes,
+                                               8 * C::kRowBytes, kSw);
+            ptx::mma_ts(wbase + 128, wbase + sb * 64 + kk * 8, bd, idO, (!pfirst[w] || kk > 0) ? 1u : 0u);
+          }
+          ptx::tc_commit(&s_free[w * 2 + sb]);
+          ptx::tc_commit(&kv_empty[pks[w]]);
+          trace(p, kTrPV, ptc[w] * 4 + w);
         }
-        if (++qs == 2) { qs = 0; qph ^= 1; }
+        pn = 0;
+      };
+      for (long long s0 = W.t0; s0 < W.t1; s0 = W.seg_end(s0)) {
+        const long long s1 = W.seg_end(s0);
+        for (long long a = s0; a < s1; a += NWG) {
+          const int np = (int)min((long long)NWG, s1 - a);
+          for (int j = 0; j < p.nKT; ++j) {
+            int cks[NWG];
+            uint32_t ctc[NWG];
+#pragma unroll
+            for (int w = 0; w < NWG; ++w) {
+              if (w >= np) break;
+              const uint32_t qs = qc[w] & 1;
+              if (j == 0) ptx::mbar_wait_spin(&q_full[w * 2 + qs], (qc[w] >> 1) & 1);
+              const uint32_t sb = tc[w] & 1;
+              ptx::mbar_wait_spin(&kv_full[ks], kph);
+              ptx::mbar_wait_spin(&s_free[w * 2 + sb], ((tc[w] >> 1) & 1) ^ 1);
+              ptx::tc_fence_after();
+              const uint32_t qbase = ptx::smem_u32(sQ + (w * 2 + qs) * C::kTileQ);
+              const uint32_t kbase = ptx::smem_u32(sK + ks * C::kTileKV);
+#pragma unroll
+              for (int kk = 0; kk < D / 16; ++kk) {
+                const uint64_t ad = ptx::smem_desc(qbase + kk * 32, 16, 8 * C::kRowBytes, kSw);
+                const uint64_t bd = ptx::smem_desc(kbase + kk * 32, 16, 8 * C::kRowBytes, kSw);
+                ptx::mma_ss(tmem + w * C::kWGcols + sb * 64, ad, bd, idS, kk > 0);
+              }
+              ptx::tc_commit(&s_full[w * 2 + sb]);
+              trace(p, kTrS, tc[w] * 4 + w);
+              if (j == p.nKT - 1) {
+                ptx::tc_commit(&q_empty[w * 2 + qs]);
+                ++qc[w];
+              }
+              cks[w] = ks;
+              ctc[w] = tc[w];
+              ++tc[w];
+              if (++ks == C::kStages) { ks = 0; kph ^= 1; }
+            }
+            issue_pvs();
+            pn = np;
+#pragma unroll
+            for (int w = 0; w < NWG; ++w) {
+              if (w >= np) break;
+              pks[w] = cks[w];
+              ptc[w] = ctc[w];
+              pfirst[w] = (j == 0);
+            }
+          }
+        }
       }
-      if (pend) issue_pv(pt, pks);
+      issue_pvs();
     }
   } else {
-    // ===================================================== softmax warpgroup
-    const int q4 = warp & 3;                 // TMEM lane quadrant of this warp
-    const int r = q4 * 32 + lane;            // query row within the tile / TMEM lane
-    const uint32_t lane_base = tmem + ((uint32_t)(q4 * 32) << 16);
-    const int tid_sm = (warp - 2) * 32 + lane;  // 0..127 for cooperative smem fills
-    long long tt = 0;
+    // ===================================================== softmax warpgroups
+    const int wg = (warp - 2) / 4;
+    const int q4 = warp & 3;                  // TMEM lane quadrant
+    const int r = q4 * 32 + lane;             // query row in tile == TMEM lane
+    const int tid_wg = (warp - 2 - 4 * wg) * 32 + lane;
+    const uint32_t lane_off = (uint32_t)(q4 * 32) << 16;
+    const uint32_t tbase = tmem + lane_off + wg * C::kWGcols;
+    const uint32_t o_tmem = tbase + 128;
+    const uint32_t bias_addr = ptx::smem_u32(sBias) + r * 128;
+    const uint32_t r7 = (uint32_t)(r & 7) << 4;  // 128B swizzle: chunk c of row r -> (c ^ (r & 7))
+    const float2 scl2 = make_float2(p.scale_log2, p.scale_log2);
+    const float2 lg2 = make_float2(kLog2e, kLog2e);
+    uint32_t qc = 0, tcount = 0;
     int bslot = 0; uint32_t bph = 0;
-    for (long long t = t0; t < t1; ++t) {
-      int ob, h, qt, n;
-      decode_item(t, p.N, p.nQT, p.H, ob, h, qt, n);
-      const int b = ob * p.N + n;
-      const int i = qt * kBM + r;
-      // stage bias1[b, :] * log2e in shared memory (fp32), keys >= L masked to -inf
-      ptx::named_bar_sync(1, 128);
-      for (int j = tid_sm; j < p.nKT * kBN; j += 128) {
-        float v = -INFINITY;
-        if (j < p.L) v = p.bias1 ? load_half<F16>(p.bias1, (size_t)b * p.L + j) * kLog2e : 0.f;
-        sB1[j] = v;
-      }
-      ptx::named_bar_sync(1, 128);
+
+    for (long long s0 = W.t0; s0 < W.t1; s0 = W.seg_end(s0)) {
+      const long long s1 = W.seg_end(s0);
+      const SegInfo si = seg_info(s0, p);
+      const int i = si.qt * kBM + r;
       const uint16_t* b2row = nullptr;
-      if (p.bias_mode == kBiasGlobal)
-        b2row = (const uint16_t*)p.bias2 + (((size_t)ob * p.H + h) * p.L + min(i, p.L - 1)) * (size_t)p.L;
-
-      float m_run = -INFINITY, l_run = 0.f, alpha_prev = 0.f;
-      float acc[D];
-#pragma unroll
-      for (int d = 0; d < D; ++d) acc[d] = 0.f;
-
-      auto fold_o = [&](long long tp, float alpha) {
-        const int sb = (int)(tp & 1);
-        ptx::mbar_wait(&o_full[sb], (uint32_t)((tp >> 1) & 1));
-        ptx::tc_fence_after();
-        constexpr int kChunk = D < 32 ? D : 32;
-#pragma unroll
-        for (int c0 = 0; c0 < D; c0 += kChunk) {
-          uint32_t ov[32];
-          if constexpr (kChunk == 16) {
-            ptx::tmem_ld16(lane_base + 256 + sb * D + c0, *(uint32_t(*)[16])ov);
-          } else {
-            ptx::tmem_ld32(lane_base + 256 + sb * D + c0, ov);
+      if constexpr (BM == kBiasGlobal)
+        b2row = (const uint16_t*)p.bias2 + (((size_t)si.ob * p.H + si.h) * p.L + min(i, p.L - 1)) * (size_t)p.L;
+      bool released = false;
+      int n = si.n0;
+      for (long long a = s0; a < s1; a += NWG, n += NWG) {
+        const int np = (int)min((long long)NWG, s1 - a);
+        if (wg >= np) {
+          // no row for this warpgroup in the segment's last group: keep the shared streamed-bias
+          // ring in step (wait each fill, then release it)
+          if (streamed) {
+            for (int j = 0; j < p.nKT; ++j) {
+              ptx::mbar_wait(&bias_full[bslot], bph);
+              if (tid_wg == 0) ptx::mbar_arrive(&bias_empty[bslot]);
+              if (++bslot == p.nbias_slots) { bslot = 0; bph ^= 1; }
+            }
           }
-          ptx::tmem_ld_wait();
-#pragma unroll
-          for (int d = 0; d < kChunk; ++d) acc[c0 + d] = fmaf(acc[c0 + d], alpha, __uint_as_float(ov[d]));
+          continue;
         }
-        ptx::tc_fence_before();
-        ptx::mbar_arrive(&o_free[sb]);
-      };
+        const int b = si.ob * p.N + n + wg;
+        const bool last_row = a + NWG >= s1;
+        // ---- bias1 row -> fp32 * log2e in this warpgroup's slot; keys >= L -> -inf
+        const uint32_t qs = qc & 1;
+        float* b1s = sB1 + (wg * 2 + qs) * LP;
+        ptx::mbar_wait(&q_full[wg * 2 + qs], (qc >> 1) & 1);
+        if (tid_wg == 0 && wg == 0) trace(p, kTrRowStart, tcount);
+        ptx::named_bar_sync(1 + wg, 128);  // previous readers of this slot are done
+        const uint16_t* rawrow = sB1raw + (wg * 2 + qs) * LP;
+        for (int j = tid_wg; j < LP; j += 128) {
+          float v = -INFINITY;
+          if (j < p.L) {
+            if (!p.bias1) v = 0.f;
+            else if (p.b1_tma) {
+              const unsigned short u = rawrow[j];
+              v = (F16 ? __half2float(__ushort_as_half(u)) : __uint_as_float((uint32_t)u << 16)) * kLog2e;
+            } else {
+              v = load_half<F16>(p.bias1, (size_t)b * p.L + j) * kLog2e;
+            }
+          }
+          b1s[j] = v;
+        }
+        ptx::named_bar_sync(1 + wg, 128);
+        if (tid_wg == 0) ptx::mbar_arrive(&q_empty[wg * 2 + qs]);  // raw bias1 row consumed
+        ++qc;
+        const uint32_t b1s_addr = ptx::smem_u32(b1s);
 
-      for (int j = 0; j < p.nKT; ++j) {
-        const int sb = (int)(tt & 1);
-        ptx::mbar_wait(&s_full[sb], (uint32_t)((tt >> 1) & 1));
-        ptx::tc_fence_after();
-        // ---- S chunk by chunk (32 columns), each finished with its bias terms before the
-        //      next TMEM load is waited on:  x = S*scale*log2e + bias2*log2e + bias1*log2e
-        const int j0 = j * kBN;
-        int slot = 0;
-        if (resident) { slot = j; ptx::mbar_wait(&bias_full[slot], bph); }
-        if (streamed) { slot = bslot; ptx::mbar_wait(&bias_full[slot], bph); }
-        const uint8_t* bt = sBias + (size_t)slot * S::kBiasTileBytes;
-        const bool smem_bias = resident || streamed;
-        float x[kBN];
-#pragma unroll
-        for (int c = 0; c < 4; ++c) {
-          uint32_t rr[32];
-          ptx::tmem_ld32(lane_base + sb * 128 + c * 32, rr);
+        float m_run = -INFINITY, l_run = 0.f;
+        for (int j = 0; j < p.nKT; ++j) {
+          const uint32_t sb = tcount & 1;
+          const uint32_t s_tmem = tbase + sb * 64;
+          ptx::mbar_wait(&s_full[wg * 2 + sb], (tcount >> 1) & 1);
+          if (tid_wg == 0 && wg == 0) trace(p, kTrSseen, tcount);
+          ptx::tc_fence_after();
+          uint32_t ra[32], rb[32];
+          ptx::tmem_ld32(s_tmem, ra);
+          ptx::tmem_ld32(s_tmem + 32, rb);
+          const int j0 = j * kBN;
+          int slot = 0;
+          if (resident) { slot = j; ptx::mbar_wait(&bias_full[slot], bph); }
+          if (streamed) { slot = bslot; ptx::mbar_wait(&bias_full[slot], bph); }
           ptx::tmem_ld_wait();
-          const float4* b1v = (const float4*)(sB1 + j0 + c * 32);
-          if (smem_bias) {
+          auto sv = [&](int k) { return __uint_as_float(k < 32 ? ra[k & 31] : rb[k & 31]); };
+          // ---- x = S*scale*log2e + bias2*log2e + bias1*log2e   (log2 domain)
+          float2 x[32];
+          if constexpr (resident || streamed) {
+            // 128B-swizzled bias tile: 8-key chunk c of row r sits at chunk c ^ (r & 7)
+            const uint32_t bt = bias_addr + slot * C::kBiasTile;
 #pragma unroll
-            for (int q = 0; q < 4; ++q) {
-              const int cc = c * 4 + q;  // 16-byte chunk (8 keys) within the 128-key row
-              const uint8_t* rowp = bt + (cc >> 3) * 16384 + r * 128;
-              const uint4 raw = *(const uint4*)(rowp + (((cc & 7) ^ (r & 7)) << 4));
-              const float4 bb0 = b1v[q * 2], bb1 = b1v[q * 2 + 1];
-              const float b1f[8] = {bb0.x, bb0.y, bb0.z, bb0.w, bb1.x, bb1.y, bb1.z, bb1.w};
-              const uint32_t w[4] = {raw.x, raw.y, raw.z, raw.w};
+            for (int c = 0; c < 8; ++c) {
+              const uint4 raw = lds128(bt + ((uint32_t)(c << 4) ^ r7));
+              const uint4 w0 = lds128(b1s_addr + (j0 + c * 8) * 4);
+              const uint4 w1 = lds128(b1s_addr + (j0 + c * 8 + 4) * 4);
+              const uint32_t wv[4] = {raw.x, raw.y, raw.z, raw.w};
+              const uint32_t bw[8] = {w0.x, w0.y, w0.z, w0.w, w1.x, w1.y, w1.z, w1.w};
 #pragma unroll
-              for (int e = 0; e < 8; ++e) {
-                const uint32_t hv = (w[e >> 1] >> ((e & 1) * 16)) & 0xFFFF;
-                const float bv = F16 ? __half2float(__ushort_as_half((unsigned short)hv)) : __uint_as_float(hv << 16);
-                x[c * 32 + q * 8 + e] = fmaf(__uint_as_float(rr[q * 8 + e]), p.scale_log2, fmaf(bv, kLog2e, b1f[e]));
+              for (int e = 0; e < 4; ++e) {
+                const float2 bb = __ffma2_rn(unpack2<F16>(wv[e]), lg2,
+                                             make_float2(__uint_as_float(bw[2 * e]), __uint_as_float(bw[2 * e + 1])));
+                x[c * 4 + e] = __ffma2_rn(make_float2(sv(c * 8 + 2 * e), sv(c * 8 + 2 * e + 1)), scl2, bb);
               }
             }
-          } else if (b2row) {
+          } else if constexpr (BM == kBiasGlobal) {
 #pragma unroll
-            for (int k = 0; k < 32; ++k) {
-              const int jj = min(j0 + c * 32 + k, p.L - 1);
-              const uint32_t hv = b2row[jj];
-              const float bv = F16 ? __half2float(__ushort_as_half((unsigned short)hv)) : __uint_as_float(hv << 16);
-              x[c * 32 + k] = fmaf(__uint_as_float(rr[k]), p.scale_log2, fmaf(bv, kLog2e, sB1[j0 + c * 32 + k]));
+            for (int k = 0; k < kBN; k += 2) {
+              const int ja = min(j0 + k, p.L - 1), jb = min(j0 + k + 1, p.L - 1);
+              const float2 bv = make_float2(load_half<F16>(b2row, ja), load_half<F16>(b2row, jb));
+              const float2 b1v = make_float2(b1s[j0 + k], b1s[j0 + k + 1]);
+              x[k / 2] = __ffma2_rn(make_float2(sv(k), sv(k + 1)), scl2, __ffma2_rn(bv, lg2, b1v));
             }
           } else {
 #pragma unroll
-            for (int k = 0; k < 32; k += 4) {
-              const float4 bb = b1v[k / 4];
-              x[c * 32 + k] = fmaf(__uint_as_float(rr[k]), p.scale_log2, bb.x);
-              x[c * 32 + k + 1] = fmaf(__uint_as_float(rr[k + 1]), p.scale_log2, bb.y);
-              x[c * 32 + k + 2] = fmaf(__uint_as_float(rr[k + 2]), p.scale_log2, bb.z);
-              x[c * 32 + k + 3] = fmaf(__uint_as_float(rr[k + 3]), p.scale_log2, bb.w);
+            for (int k = 0; k < kBN; k += 4) {
+              const uint4 wu = lds128(b1s_addr + (j0 + k) * 4);
+              x[k / 2] = __ffma2_rn(make_float2(sv(k), sv(k + 1)), scl2,
+                                    make_float2(__uint_as_float(wu.x), __uint_as_float(wu.y)));
+              x[k / 2 + 1] = __ffma2_rn(make_float2(sv(k + 2), sv(k + 3)), scl2,
+                                        make_float2(__uint_as_float(wu.z), __uint_as_float(wu.w)));
             }
           }
-        }
-        if (streamed) {
-          ptx::mbar_arrive(&bias_empty[slot]);
-          if (++bslot == p.nbias_slots) { bslot = 0; bph ^= 1; }
-        }
-        // resident bias: release all tiles right after the last use of this unit (before the
-        // O fold, which waits on an MMA that is only issued once the next unit is loading)
-        if (resident && j == p.nKT - 1 && (t + 1 == t1 || (t + 1) / p.N != t / p.N)) {
-          for (int s2 = 0; s2 < p.nKT; ++s2) ptx::mbar_arrive(&bias_empty[s2]);
-          bph ^= 1;
-        }
-        // ---- online max / exp / sum
-        float mt = x[0];
+          // ---- bias release: streamed tiles per use; the resident block after the segment's last use
+          if (streamed || (resident && last_row && j == p.nKT - 1)) {
+            ptx::named_bar_sync(1 + wg, 128);
+            if (tid_wg == 0) {
+              if (streamed) ptx::mbar_arrive(&bias_empty[slot]);
+              else for (int s2 = 0; s2 < p.nKT; ++s2) ptx::mbar_arrive(&bias_empty[s2]);
+            }
+            released = true;
+          }
+          if (streamed && ++bslot == p.nbias_slots) { bslot = 0; bph ^= 1; }
+          // ---- tile max; lazy rescale of the running max and O
+          float mx[4];
 #pragma unroll
-        for (int c = 1; c < kBN; ++c) mt = fmaxf(mt, x[c]);
-        const float m_new = fmaxf(m_run, mt);
-        const float base = m_new == -INFINITY ? 0.f : m_new;
-        const float alpha = ex2(m_run - base);
-        float sum = 0.f;
-        uint32_t pk0[32], pk1[32];
+          for (int k = 0; k < 4; ++k) mx[k] = fmaxf(x[k].x, x[k].y);
 #pragma unroll
-        for (int c = 0; c < kBN / 2; c += 2) {
-          const float p0 = ex2(x[c] - base), p1 = ex2(x[c + 1] - base);
-          sum += p0 + p1;
-          pk0[c / 2] = F16 ? ptx::pack_f16(p0, p1) : ptx::pack_bf16(p0, p1);
-        }
-        ptx::tmem_st32(lane_base + sb * 128, pk0);
+          for (int k = 4; k < 32; ++k) mx[k & 3] = fmaxf(mx[k & 3], fmaxf(x[k].x, x[k].y));
+          const float mt = fmaxf(fmaxf(mx[0], mx[1]), fmaxf(mx[2], mx[3]));
+          const bool grow = mt > m_run + kRescaleThreshold;  // also true for the first finite tile
+          if (__any_sync(0xffffffffu, grow)) {
+            const float m_new = grow ? mt : m_run;
+            const float alpha = ex2(m_run - (m_new == -INFINITY ? 0.f : m_new));  // 0 when m_run=-inf
+            l_run *= alpha;
+            if (j > 0) {
+              // O holds the PVs of earlier tiles: wait for the last one, scale these rows in TMEM
+              const uint32_t tp = tcount - 1;
+              ptx::mbar_wait(&s_free[wg * 2 + (tp & 1)], (tp >> 1) & 1);
+              ptx::tc_fence_after();
 #pragma unroll
-        for (int c = kBN / 2; c < kBN; c += 2) {
-          const float p0 = ex2(x[c] - base), p1 = ex2(x[c + 1] - base);
-          sum += p0 + p1;
-          pk1[c / 2 - 32] = F16 ? ptx::pack_f16(p0, p1) : ptx::pack_bf16(p0, p1);
+              for (int c0 = 0; c0 < D; c0 += 16) {
+                uint32_t ov[16];
+                ptx::tmem_ld16(o_tmem + c0, ov);
+                ptx::tmem_ld_wait();
+#pragma unroll
+                for (int d = 0; d < 16; ++d) ov[d] = __float_as_uint(__uint_as_float(ov[d]) * alpha);
+                ptx::tmem_st16(o_tmem + c0, ov);
+              }
+            }
+            m_run = m_new;
+          }
+          const float base = m_run == -INFINITY ? 0.f : m_run;
+          const float2 nb = make_float2(-base, -base);
+          float2 sum[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
+          uint32_t pk[32];
+#pragma unroll
+          for (int k = 0; k < 32; ++k) {
+            float2 t = __fadd2_rn(x[k], nb);
+            t.x = ex2(t.x);
+            t.y = ex2(t.y);
+            sum[k & 1] = __fadd2_rn(sum[k & 1], t);
+            pk[k] = F16 ? ptx::pack_f16(t.x, t.y) : ptx::pack_bf16(t.x, t.y);
+          }
+          ptx::tmem_st32(s_tmem, pk);  // P (bf16) over the first 32 columns of this S buffer
+          const float2 s01 = __fadd2_rn(sum[0], sum[1]);
+          l_run += s01.x + s01.y;
+          ptx::tmem_st_wait();
+          ptx::tc_fence_before();
+          ptx::mbar_arrive(&p_full[wg * 2 + sb]);
+          if (tid_wg == 0) trace(p, wg == 0 ? kTrP0 : kTrP1, tcount);
+          ++tcount;
         }
-        ptx::tmem_st32(lane_base + sb * 128 + 32, pk1);
-        l_run = l_run * alpha + sum;
-        m_run = m_new;
-        ptx::tmem_st_wait();
+        // ---- row end: O = O / l, LSE = (m + log2 l) * ln 2
+        const uint32_t tl = tcount - 1;
+        ptx::mbar_wait(&s_free[wg * 2 + (tl & 1)], (tl >> 1) & 1);  // last PV of the row done
+        ptx::tc_fence_after();
+        uint32_t ov[D];
+#pragma unroll
+        for (int c0 = 0; c0 < D; c0 += 16) ptx::tmem_ld16(o_tmem + c0, *(uint32_t(*)[16])(&ov[c0]));
+        ptx::tmem_ld_wait();
         ptx::tc_fence_before();
-        ptx::mbar_arrive(&p_full[sb]);
-        // ---- fold the previous tile's O_j into the register accumulator
-        if (j > 0) fold_o(tt - 1, alpha_prev);
-        alpha_prev = alpha;
-        if (j == p.nKT - 1) fold_o(tt, alpha);
-        ++tt;
+        ptx::mbar_arrive(&o_free[wg]);
+        if (tid_wg == 0 && wg == 0) trace(p, kTrRowEnd, tl);
+        if (i < p.L) {
+          const float inv = l_run > 0.f ? __frcp_rn(l_run) : 0.f;
+          uint32_t ow[D / 2];
+#pragma unroll
+          for (int d = 0; d < D; d += 2) {
+            const float o0 = __uint_as_float(ov[d]) * inv, o1 = __uint_as_float(ov[d + 1]) * inv;
+            ow[d / 2] = F16 ? ptx::pack_f16(o0, o1) : ptx::pack_bf16(o0, o1);
+          }
+          uint4* dst = (uint4*)((uint16_t*)p.o + (((size_t)b * p.L + i) * p.H + si.h) * D);
+#pragma unroll
+          for (int v = 0; v < D / 8; ++v) dst[v] = make_uint4(ow[4 * v], ow[4 * v + 1], ow[4 * v + 2], ow[4 * v + 3]);
+          p.lse[((size_t)b * p.H + si.h) * p.L + i] = l_run > 0.f ? (m_run + __log2f(l_run)) * kLn2 : -INFINITY;
+        }
       }
-      // ---- epilogue: O = acc / l, LSE = (m + log2 l) * ln 2
-      if (i < p.L) {
-        const float inv = l_run > 0.f ? 1.f / l_run : 0.f;
-        uint32_t ow[D / 2];
-#pragma unroll
-        for (int d = 0; d < D; d += 2)
-          ow[d / 2] = F16 ? ptx::pack_f16(acc[d] * inv, acc[d + 1] * inv) : ptx::pack_bf16(acc[d] * inv, acc[d + 1] * inv);
-        uint4* dst = (uint4*)((uint16_t*)p.o + (((size_t)b * p.L + i) * p.H + h) * D);
-#pragma unroll
-        for (int v = 0; v < D / 8; ++v) dst[v] = make_uint4(ow[4 * v], ow[4 * v + 1], ow[4 * v + 2], ow[4 * v + 3]);
-        p.lse[((size_t)b * p.H + h) * p.L + i] = l_run > 0.f ? (m_run + __log2f(l_run)) * kLn2 : -INFINITY;
+      if (resident) {
+        // a warpgroup with no row in this segment still owes its release: wait for the fill first
+        if (!released) {
+          for (int s2 = 0; s2 < p.nKT; ++s2) ptx::mbar_wait(&bias_full[s2], bph);
+          if (tid_wg == 0)
+            for (int s2 = 0; s2 < p.nKT; ++s2) ptx::mbar_arrive(&bias_empty[s2]);
+        }
+        bph ^= 1;
       }
     }
   }

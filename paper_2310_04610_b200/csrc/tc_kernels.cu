@@ -12,6 +12,8 @@
 namespace evo {
 namespace tc {
 
+unsigned long long* g_trace = nullptr;
+
 namespace {
 
 PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
@@ -49,7 +51,7 @@ bool map_bl_hd(CUtensorMap* m, const void* base, const Shape& s, int rows, CUten
   cuuint32_t box[4] = {(cuuint32_t)s.D, 1, (cuuint32_t)rows, 1};
   cuuint32_t es[4] = {1, 1, 1, 1};
   CUresult r = encode_fn()(m, dt, 4, const_cast<void*>(base), dims, strides, box, es,
-                           CU_TENSOR_MAP_INTERLEAVE_NONE, swz(s.D * esize), CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                           CU_TENSOR_MAP_INTERLEAVE_NONE, swz(s.D * esize), CU_TENSOR_MAP_L2_PROMOTION_NONE,
                            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) {
     *err = "cuTensorMapEncodeTiled (B,L,H,D) failed: " + std::to_string((int)r);
@@ -63,7 +65,7 @@ bool map_bias(CUtensorMap* m, const void* base, const Shape& s, int Bo, CUtensor
               std::string* err) {
   cuuint64_t dims[3] = {(cuuint64_t)s.L, (cuuint64_t)s.L, (cuuint64_t)Bo * s.H};
   cuuint64_t strides[2] = {(cuuint64_t)s.L * 2, (cuuint64_t)s.L * s.L * 2};
-  cuuint32_t box[3] = {64, 128, 1};
+  cuuint32_t box[3] = {kBN, kBM, 1};
   cuuint32_t es[3] = {1, 1, 1};
   CUresult r = encode_fn()(m, dt, 3, const_cast<void*>(base), dims, strides, box, es,
                            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
@@ -77,12 +79,13 @@ bool map_bias(CUtensorMap* m, const void* base, const Shape& s, int Bo, CUtensor
 
 template <int D>
 size_t fwd_smem_bytes(int nbias_slots, int nKT) {
-  using S = FwdSmem<D>;
+  using C = FwdCfg<D>;
+  const size_t LP = (size_t)nKT * kBN;
   size_t b = 1024;  // alignment slack
-  b += 2 * S::kTileBytes + 2 * S::kStages * S::kTileBytes;
-  b += (size_t)nbias_slots * S::kBiasTileBytes;
-  b += (size_t)nKT * kBN * 4;
-  b += (4 + 2 * S::kStages + 10 + 2 * nbias_slots) * 8 + 16;
+  b += (size_t)C::NWG * 2 * C::kTileQ + 2 * (size_t)C::kStages * C::kTileKV;
+  b += (size_t)nbias_slots * C::kBiasTile;
+  b += (size_t)C::NWG * 2 * LP * (2 + 4);  // bias1 row: raw bf16 + fp32, double buffered per WG
+  b += (size_t)(11 * C::NWG + 2 * C::kStages + 2 * nbias_slots) * 8 + 16;
   return b;
 }
 
@@ -107,8 +110,10 @@ evo_status launch_fwd(const evo_attn_desc* d, const Shape& s, const void* q, con
   p.bias2 = s.bias2;
   p.o = o;
   p.lse = lse;
+  p.trace = g_trace;
   p.bias_mode = kBiasNone;
   p.nbias_slots = 0;
+  p.b1_tma = (s.L % 8 == 0) ? 1 : 0;
   if (s.bias2) {
     if (s.L % 8 != 0) {
       p.bias_mode = kBiasGlobal;
@@ -119,7 +124,7 @@ evo_status launch_fwd(const evo_attn_desc* d, const Shape& s, const void* q, con
         p.nbias_slots = p.nKT;
       } else {
         p.bias_mode = kBiasStreamed;
-        p.nbias_slots = 2;
+        p.nbias_slots = 3;
       }
     }
   }
@@ -128,10 +133,25 @@ evo_status launch_fwd(const evo_attn_desc* d, const Shape& s, const void* q, con
     *err = "forward shared-memory budget exceeded (L too large)";
     return EVO_ERR_UNSUPPORTED;
   }
-  auto kern = fwd_kernel<D, F16>;
+  auto kern = p.bias_mode == kBiasResident   ? fwd_kernel<D, F16, kBiasResident>
+              : p.bias_mode == kBiasStreamed ? fwd_kernel<D, F16, kBiasStreamed>
+              : p.bias_mode == kBiasGlobal   ? fwd_kernel<D, F16, kBiasGlobal>
+                                             : fwd_kernel<D, F16, kBiasNone>;
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  const long long grid = std::min<long long>(p.total, sm_count());
-  kern<<<(unsigned)grid, kFwdThreads, smem, st>>>(tq, tk, tv, tb, p);
+  // Grid: one CTA per SM. If every (ob, h, q-tile) unit can get >= 4 CTAs, give each unit the same
+  // number of CTAs with aligned row ranges (the q-tiles of a row then run concurrently and share
+  // K/V through L2); otherwise split the flat item list evenly over the SMs.
+  const int G = sm_count();
+  const long long units = (long long)p.Bo * p.H * p.nQT;
+  long long grid = std::min<long long>(p.total, G);
+  p.aligned = 0;
+  p.split = 1;
+  if (units * 4 <= G) {
+    p.split = (int)std::min<long long>(G / units, p.N);
+    p.aligned = 1;
+    grid = units * p.split;
+  }
+  kern<<<(unsigned)grid, FwdCfg<D>::kThreads, smem, st>>>(tq, tk, tv, tb, p);
   ++*launches;
   return EVO_OK;
 }
@@ -180,3 +200,7 @@ evo_status fwd(const evo_attn_desc* d, const Shape& s, const void* q, const void
 
 }  // namespace tc
 }  // namespace evo
+
+// Bring-up aid (not part of include/evoattn.h): record a clock64 timeline of CTA 0 of the next
+// forward launches into a device buffer of 8 x 64 uint64 (null disables).
+extern "C" void evo_attn_debug_set_trace(void* dev_buf) { evo::tc::g_trace = (unsigned long long*)dev_buf; }
