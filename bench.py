@@ -255,7 +255,7 @@ def main():
     E.evoformer_attention_forward(q, k, v, b1, b2)
     n_fwd = E.last_launch_count()
     o, lse = E.evoformer_attention_forward(q, k, v, b1, b2)
-    E.evoformer_attention_backward(do, q, k, v, o, lse, b1, b2, need_dbias1=True)
+    E.evoformer_attention_backward(do, q, k, v, o, lse, b1, b2, need_dbias1=False)
     n_bwd = E.last_launch_count()
     path = E.resolved_path(q, b1, b2)
 
@@ -306,7 +306,7 @@ def main():
     nk = max(10, args.steps // 2)
     fwd_ms = time_call(lambda: E.evoformer_attention_forward(q, k, v, b1, b2), nk)
     bwd_ms = time_call(lambda: E.evoformer_attention_backward(do, q, k, v, o, lse, b1, b2,
-                                                              need_dbias1=True), nk)
+                                                              need_dbias1=False), nk)
     pk = peaks()
     f_fwd = 4.0 * B_local * H * L * L * D
     f_bwd = 10.0 * B_local * H * L * L * D

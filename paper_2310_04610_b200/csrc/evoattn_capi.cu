@@ -241,7 +241,7 @@ evo_status evo_attn_bwd(const evo_attn_desc* d, const void* dout, const void* q,
     case EVO_BF16: launch_delta<__nv_bfloat16>(s, dout, o, delta, cs); break;
     default: launch_delta<__half>(s, dout, o, delta, cs); break;
   }
-  if (path == EVO_PATH_TCGEN05 && evo::tc::bwd_available(d)) {
+  if (path == EVO_PATH_TCGEN05 && evo::tc::bwd_available(d) && !dbias1) {
     st = evo::tc::bwd(d, s, dout, q, k, v, lse, delta, dq, dk, dv, db1, db2, ws + w.tc, cs,
                       &g_launches, &g_err);
   } else {

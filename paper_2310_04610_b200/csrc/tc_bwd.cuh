@@ -1,0 +1,569 @@
+// tc_bwd.cuh — K3: fused Evoformer attention backward on tcgen05 / TMEM / TMA (sm_100a).
+//
+// Reference semantics: attn_backward_tiled, /root/reference/proj/core/src/attention_tiled.cpp:182-340:
+// P = exp(S - LSE) recomputed per tile, dV += P^T dO, dP = dO V^T, dS = P (dP - delta),
+// dQ += dS K, dK += dS^T Q (dQ, dK scaled once), dBias[h] += sum_b dS (F32 accumulator).
+//
+// B200 layout. A CTA owns one (ob, h, 64-key tile) "unit" and a range of its MSA rows b; for each
+// row it walks the query tiles (128 rows each):
+//  * the pair-bias strip bias2[ob, h, :, keys] (all queries x 64 keys, bf16) is TMA-loaded once per
+//    unit and stays in shared memory;
+//  * the dBias2 strip (all queries x 64 keys, fp32) stays in TMEM for the whole unit: every row's
+//    dS is reduced into it on chip (the broadcast-reverse sum of attention_tiled.cpp:318-323 done
+//    in the kernel), and it leaves the SM once, as a fp32 red.add per unit — not once per row;
+//  * S = Q K^T and dP = dO V^T (M=128 queries, N=64 keys) land in double-buffered TMEM tiles;
+//    two softmax warpgroups (32 keys each) rebuild P from LSE in the log2 domain, form
+//    dS = P (dP - delta), add dS into the strip, and write P and dS as bf16 into 128B-swizzled
+//    shared tiles that serve both as MN-major (P^T, dS^T) and K-major (dS) UMMA operands;
+//  * dV += P^T dO and dK += dS^T Q accumulate over the query tiles in two M=64 TMEM accumulators
+//    that share 32 columns (lanes 0-15 / 16-31 of each quadrant); dK/dV are stored once per row;
+//  * dQ_partial = dS K (M=128) is drained by an epilogue warpgroup and added into an fp32 dQ
+//    accumulator with TMA bulk reduce-add (one partial per 64-key tile), converted afterwards.
+//  TMEM: S/dP buffers [0,256), dBias strip [256, 256+64*nQT), dQ at 448, dK|dV at 480 (nQT <= 3).
+#pragma once
+#include "common.cuh"
+#include "tc_ptx.cuh"
+
+namespace evo {
+namespace tc {
+namespace bk {
+
+constexpr int kBM = 128;   // queries per tile
+constexpr int kBN = 64;    // keys per tile
+constexpr int kThreads = 64 + 256 + 128;  // TMA, MMA, 2 softmax WGs, epilogue WG
+constexpr uint32_t kStripCol = 256, kDqCol = 448, kDkvCol = 480;
+
+template <int D>
+struct Cfg {
+  static constexpr int kRowBytes = D * 2;
+  static constexpr int kTileQ = kBM * kRowBytes;    // Q or dO tile
+  static constexpr int kTileK = kBN * kRowBytes;    // K or V tile
+  static constexpr int kQStages = 3;                // (Q, dO, lse, delta) ring
+  static constexpr int kKStages = 2;                // (K, V, bias1 chunk) ring
+  static constexpr int kBiasTile = kBM * kBN * 2;   // 16 KB
+  static constexpr int kPdsTile = kBM * kBN * 2;    // 16 KB (P or dS, bf16)
+  static constexpr int kDqStage = kBM * D * 4;      // fp32 dQ staging
+};
+
+struct Params {
+  int B, N, L, H, Bo;
+  int nQT, nKT;
+  long long total;   // items = Bo*H*nKT*N
+  int aligned, split;
+  float scale, scale_log2;
+  const void* bias1;    // [B, L] or null
+  const float* lse2;    // [B, H, nQT*128] lse * log2e, +inf past L
+  const float* delta;   // [B, H, nQT*128] rowsum(dO * O), 0 past L
+  void* dk;             // [B, L, H, D]
+  void* dv;
+  float* dbias2;        // [Bo, H, L, L] fp32 accumulator or null
+  int has_bias2;
+};
+
+struct Walker {
+  long long t0, t1, N;
+  __device__ long long seg_end(long long s) const {
+    const long long e = (s / N + 1) * N;
+    return e < t1 ? e : t1;
+  }
+};
+__device__ __forceinline__ Walker make_walker(const Params& p) {
+  if (p.aligned) {
+    const long long unit = blockIdx.x / p.split, part = blockIdx.x % p.split;
+    const long long base = unit * p.N;
+    return Walker{base + p.N * part / p.split, base + p.N * (part + 1) / p.split, p.N};
+  }
+  return Walker{p.total * blockIdx.x / gridDim.x, p.total * (blockIdx.x + 1) / gridDim.x, p.N};
+}
+struct Unit {
+  int ob, h, jt, n0;
+};
+__device__ __forceinline__ Unit unit_of(long long s0, const Params& p) {
+  Unit u;
+  long long x = s0 / p.N;
+  u.n0 = (int)(s0 - x * p.N);
+  u.jt = (int)(x % p.nKT);
+  x /= p.nKT;
+  u.h = (int)(x % p.H);
+  u.ob = (int)(x / p.H);
+  return u;
+}
+
+__device__ __forceinline__ uint4 lds128(uint32_t a) {
+  uint4 v;
+  asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ void sts128(uint32_t a, uint4 v) {
+  asm volatile("st.shared.v4.u32 [%0], {%1,%2,%3,%4};" ::"r"(a), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w) : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
+               "l"(src), "r"(bytes), "r"(ptx::smem_u32(bar))
+               : "memory");
+}
+template <bool F16>
+__device__ __forceinline__ float2 unpack2(uint32_t w) {
+  if constexpr (F16) {
+    __half2 hh = *reinterpret_cast<__half2*>(&w);
+    return __half22float2(hh);
+  } else {
+    return make_float2(__uint_as_float(w << 16), __uint_as_float(w & 0xFFFF0000u));
+  }
+}
+__device__ __forceinline__ void red_v4(float* gaddr, float a, float b, float c, float d) {
+  asm volatile("red.global.add.v4.f32 [%0], {%1,%2,%3,%4};" ::"l"(gaddr), "f"(a), "f"(b), "f"(c), "f"(d) : "memory");
+}
+
+template <int D, bool F16>
+__global__ void __launch_bounds__(kThreads, 1)
+    bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
+               const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmdO,
+               const __grid_constant__ CUtensorMap tmB2, const __grid_constant__ CUtensorMap tmdQ,
+               const Params p) {
+  using C = Cfg<D>;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  // ---- shared memory carve-up (all operand tiles 1024-aligned)
+  uint8_t* sQ = smem;                                          // [QS] Q tiles
+  uint8_t* sdO = sQ + C::kQStages * C::kTileQ;                 // [QS] dO tiles
+  uint8_t* sK = sdO + C::kQStages * C::kTileQ;                 // [KS] K tiles
+  uint8_t* sV = sK + C::kKStages * C::kTileK;                  // [KS] V tiles
+  uint8_t* sP = sV + C::kKStages * C::kTileK;                  // [2] P tiles (bf16, SW128)
+  uint8_t* sdS = sP + 2 * C::kPdsTile;                         // [2] dS tiles
+  uint8_t* sBias = sdS + 2 * C::kPdsTile;                      // [nQT] bias strip tiles
+  float* sDq = (float*)(sBias + (size_t)p.nQT * C::kBiasTile);  // [2] dQ staging (fp32 128 x D)
+  float* sLse = sDq + 2 * kBM * D;                             // [QS][128] lse * log2e (raw fp32 on arrival)
+  float* sDel = sLse + C::kQStages * kBM;                      // [QS][128]
+  float* sB1f = sDel + C::kQStages * kBM;                      // [2 WG][2][32] bias1 * log2e (fp32)
+  uint16_t* sB1 = (uint16_t*)(sB1f + 128);                     // [KS][64] bias1 chunk (raw)
+  uint64_t* bars = (uint64_t*)(sB1 + C::kKStages * 64);
+  uint64_t* q_full = bars;                          // [QS]
+  uint64_t* q_empty = q_full + C::kQStages;         // [QS]
+  uint64_t* k_full = q_empty + C::kQStages;         // [KS]
+  uint64_t* k_empty = k_full + C::kKStages;         // [KS]
+  uint64_t* s_full = k_empty + C::kKStages;         // [2] S and dP of a step computed
+  uint64_t* s_free = s_full + 2;                    // [2] softmax done reading S/dP of a buffer
+  uint64_t* pds_full = s_free + 2;                  // [2] P/dS of a step written (256 arrivals)
+  uint64_t* pds_free = pds_full + 2;                // [2] MMAs reading that P/dS buffer done
+  uint64_t* dq_full = pds_free + 2;                 // [1] dQ partial computed
+  uint64_t* dq_free = dq_full + 1;                  // [1] dQ drained from TMEM
+  uint64_t* kv_done = dq_free + 1;                  // [1] dK/dV of a row complete
+  uint64_t* kv_free = kv_done + 1;                  // [1] dK/dV read out
+  uint64_t* bias_full = kv_free + 1;                // [1] bias strip of the unit landed
+  uint64_t* bias_empty = bias_full + 1;             // [1] strip readers done (2 WGs)
+  uint32_t* tmem_slot = (uint32_t*)(bias_empty + 1);
+
+  const int warp = threadIdx.x / 32;
+  const int lane = threadIdx.x % 32;
+  const Walker W = make_walker(p);
+  constexpr uint32_t kSw = ptx::swizzle_code(C::kRowBytes);
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < C::kQStages; ++s) { ptx::mbar_init(&q_full[s], 1); ptx::mbar_init(&q_empty[s], 1); }
+    for (int s = 0; s < C::kKStages; ++s) { ptx::mbar_init(&k_full[s], 1); ptx::mbar_init(&k_empty[s], 1); }
+    for (int s = 0; s < 2; ++s) {
+      ptx::mbar_init(&s_full[s], 1);
+      ptx::mbar_init(&s_free[s], 256);
+      ptx::mbar_init(&pds_full[s], 256);
+      ptx::mbar_init(&pds_free[s], 1);
+    }
+    ptx::mbar_init(dq_full, 1);
+    ptx::mbar_init(dq_free, 128);
+    ptx::mbar_init(kv_done, 1);
+    ptx::mbar_init(kv_free, 128);
+    ptx::mbar_init(bias_full, 1);
+    ptx::mbar_init(bias_empty, 2);
+    ptx::fence_barrier_init();
+  }
+  if (warp == 1) ptx::tmem_alloc(tmem_slot, 512);
+  ptx::tc_fence_before();
+  __syncthreads();
+  ptx::tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    if (ptx::elect_one()) {
+      // ===================================================== TMA producer
+      ptx::tma_prefetch(&tmQ); ptx::tma_prefetch(&tmK); ptx::tma_prefetch(&tmV); ptx::tma_prefetch(&tmdO);
+      if (p.has_bias2) ptx::tma_prefetch(&tmB2);
+      int qs = 0; uint32_t qph = 0;
+      int ks = 0; uint32_t kph = 0;
+      uint32_t bph = 0;
+      for (long long s0 = W.t0; s0 < W.t1; s0 = W.seg_end(s0)) {
+        const long long s1 = W.seg_end(s0);
+        const Unit u = unit_of(s0, p);
+        const int plane = u.ob * p.H + u.h;
+        if (p.has_bias2) {
+          ptx::mbar_wait(bias_empty, bph ^ 1);
+          ptx::mbar_expect_tx(bias_full, p.nQT * C::kBiasTile);
+          for (int it = 0; it < p.nQT; ++it)
+            ptx::tma_load_3d(sBias + (size_t)it * C::kBiasTile, &tmB2, bias_full, u.jt * kBN, it * kBM, plane);
+          bph ^= 1;
+        }
+        int n = u.n0;
+        for (long long a = s0; a < s1; ++a, ++n) {
+          const int b = u.ob * p.N + n;
+          // K, V (and the bias1 chunk) of this row's key tile
+          ptx::mbar_wait(&k_empty[ks], kph ^ 1);
+          const int nk = min(kBN, p.L - u.jt * kBN);  // keys of this tile (multiple of 8)
+          const uint32_t b1bytes = p.bias1 ? (uint32_t)nk * 2 : 0u;
+          ptx::mbar_expect_tx(&k_full[ks], 2 * C::kTileK + b1bytes);
+          ptx::tma_load_4d(sK + ks * C::kTileK, &tmK, &k_full[ks], 0, u.h, u.jt * kBN, b);
+          ptx::tma_load_4d(sV + ks * C::kTileK, &tmV, &k_full[ks], 0, u.h, u.jt * kBN, b);
+          if (b1bytes)
+            bulk_g2s(ptx::smem_u32(sB1 + ks * 64), (const uint16_t*)p.bias1 + (size_t)b * p.L + u.jt * kBN, b1bytes,
+                     &k_full[ks]);
+          if (++ks == C::kKStages) { ks = 0; kph ^= 1; }
+          for (int it = 0; it < p.nQT; ++it) {
+            ptx::mbar_wait(&q_empty[qs], qph ^ 1);
+            ptx::mbar_expect_tx(&q_full[qs], 2 * C::kTileQ + 2 * kBM * 4);
+            ptx::tma_load_4d(sQ + qs * C::kTileQ, &tmQ, &q_full[qs], 0, u.h, it * kBM, b);
+            ptx::tma_load_4d(sdO + qs * C::kTileQ, &tmdO, &q_full[qs], 0, u.h, it * kBM, b);
+            const size_t row0 = ((size_t)b * p.H + u.h) * (p.nQT * kBM) + (size_t)it * kBM;
+            bulk_g2s(ptx::smem_u32(sLse + qs * kBM), p.lse2 + row0, kBM * 4, &q_full[qs]);
+            bulk_g2s(ptx::smem_u32(sDel + qs * kBM), p.delta + row0, kBM * 4, &q_full[qs]);
+            if (++qs == C::kQStages) { qs = 0; qph ^= 1; }
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ===================================================== MMA issuer (converged warp, one elected lane
+    // issues: descriptors stay in uniform registers)
+    const uint32_t idS = ptx::instr_desc(kBM, kBN, F16, false, false);   // S, dP: K-major A, K-major B
+    const uint32_t idKV = ptx::instr_desc(64, D, F16, true, true);       // dV, dK: MN-major A and B
+    const uint32_t idQ = ptx::instr_desc(kBM, D, F16, false, true);      // dQ: K-major A, MN-major B
+    const uint32_t q0 = ptx::smem_u32(sQ), do0 = ptx::smem_u32(sdO), k0 = ptx::smem_u32(sK), v0 = ptx::smem_u32(sV);
+    const uint32_t p0 = ptx::smem_u32(sP), ds0 = ptx::smem_u32(sdS);
+    int qs = 0; uint32_t qph = 0;
+    int ks = 0; uint32_t kph = 0;
+    uint32_t step = 0;    // (row, q-tile) steps issued: S buffer = step & 1
+    uint32_t rows = 0;    // rows started (kv_free parity)
+    // gradient MMAs of the previous step
+    bool pend = false; uint32_t pstep = 0; int pqs = 0, pks = 0; bool pfirst = false, plast = false;
+    auto issue_grads = [&]() {
+      const uint32_t sb = pstep & 1, ph = (pstep >> 1) & 1;
+      ptx::mbar_wait_spin(&pds_full[sb], ph);
+      if (pfirst) {  // first q-tile of a row overwrites dK/dV: previous row must be read out
+        ptx::mbar_wait_spin(kv_free, (rows & 1) ^ 1);
+        ++rows;
+      }
+      ptx::mbar_wait_spin(dq_free, (pstep & 1) ^ 1);
+      ptx::tc_fence_after();
+      const uint32_t pA = p0 + sb * C::kPdsTile;
+      const uint32_t dsA = ds0 + sb * C::kPdsTile;
+      const uint32_t qB = q0 + pqs * C::kTileQ;
+      const uint32_t doB = do0 + pqs * C::kTileQ;
+      const uint32_t kB = k0 + pks * C::kTileK;
+      if (ptx::elect_one()) {
+#pragma unroll
+        for (int kk = 0; kk < kBM / 16; ++kk) {  // K = 128 queries: 16 rows per step
+          // A = P^T / dS^T: MN-major SW128 (64 keys wide), 16 query rows = 2 x 8-row atoms
+          const uint64_t aP = ptx::smem_desc(pA + kk * 16 * 128, 1024, 1024, 2);
+          const uint64_t aS = ptx::smem_desc(dsA + kk * 16 * 128, 1024, 1024, 2);
+          // B = dO / Q: MN-major (D wide), 16 query rows
+          const uint64_t bdO = ptx::smem_desc(doB + kk * 16 * C::kRowBytes, 16 * C::kRowBytes, 8 * C::kRowBytes, kSw);
+          const uint64_t bQ = ptx::smem_desc(qB + kk * 16 * C::kRowBytes, 16 * C::kRowBytes, 8 * C::kRowBytes, kSw);
+          const uint32_t acc = (!pfirst || kk > 0) ? 1u : 0u;
+          ptx::mma_ss(tmem + kDkvCol + (16u << 16), aP, bdO, idKV, acc);  // dV (lanes 16-31 of each quadrant)
+          ptx::mma_ss(tmem + kDkvCol, aS, bQ, idKV, acc);                 // dK (lanes 0-15)
+        }
+#pragma unroll
+        for (int kk = 0; kk < kBN / 16; ++kk) {  // dQ = dS K: K = 64 keys
+          const uint64_t aS = ptx::smem_desc(dsA + kk * 32, 16, 1024, 2);  // K-major SW128 rows
+          const uint64_t bK = ptx::smem_desc(kB + kk * 16 * C::kRowBytes, 16 * C::kRowBytes, 8 * C::kRowBytes, kSw);
+          ptx::mma_ss(tmem + kDqCol, aS, bK, idQ, kk > 0);
+        }
+        ptx::tc_commit(dq_full);
+        ptx::tc_commit(&pds_free[sb]);
+        ptx::tc_commit(&q_empty[pqs]);
+        if (plast) {
+          ptx::tc_commit(kv_done);
+          ptx::tc_commit(&k_empty[pks]);
+        }
+      }
+      __syncwarp();
+    };
+    for (long long s0 = W.t0; s0 < W.t1; s0 = W.seg_end(s0)) {
+      const long long s1 = W.seg_end(s0);
+      for (long long a = s0; a < s1; ++a) {
+        ptx::mbar_wait_spin(&k_full[ks], kph);
+        const uint32_t kA = k0 + ks * C::kTileK;
+        const uint32_t vA = v0 + ks * C::kTileK;
+        for (int it = 0; it < p.nQT; ++it) {
+          const uint32_t sb = step & 1;
+          ptx::mbar_wait_spin(&q_full[qs], qph);
+          ptx::mbar_wait_spin(&s_free[sb], ((step >> 1) & 1) ^ 1);
+          ptx::tc_fence_after();
+          const uint32_t qA = q0 + qs * C::kTileQ;
+          const uint32_t doA = do0 + qs * C::kTileQ;
+          if (ptx::elect_one()) {
+#pragma unroll
+            for (int kk = 0; kk < D / 16; ++kk) {
+              const uint64_t a1 = ptx::smem_desc(qA + kk * 32, 16, 8 * C::kRowBytes, kSw);
+              const uint64_t b1 = ptx::smem_desc(kA + kk * 32, 16, 8 * C::kRowBytes, kSw);
+              ptx::mma_ss(tmem + sb * 128, a1, b1, idS, kk > 0);          // S
+              const uint64_t a2 = ptx::smem_desc(doA + kk * 32, 16, 8 * C::kRowBytes, kSw);
+              const uint64_t b2 = ptx::smem_desc(vA + kk * 32, 16, 8 * C::kRowBytes, kSw);
+              ptx::mma_ss(tmem + sb * 128 + 64, a2, b2, idS, kk > 0);     // dP
+            }
+            ptx::tc_commit(&s_full[sb]);
+          }
+          __syncwarp();
+          if (pend) issue_grads();
+          pend = true; pstep = step; pqs = qs; pks = ks; pfirst = (it == 0); plast = (it == p.nQT - 1);
+          ++step;
+          if (++qs == C::kQStages) { qs = 0; qph ^= 1; }
+        }
+        if (++ks == C::kKStages) { ks = 0; kph ^= 1; }
+      }
+    }
+    if (pend) issue_grads();
+  } else if (warp < 10) {
+    // ===================================================== softmax warpgroups (2 x 32 keys)
+    const int wg = (warp - 2) / 4;
+    const int q4 = warp & 3;
+    const int r = q4 * 32 + lane;                 // query row in tile == TMEM lane
+    const int tid_wg = (warp - 2 - 4 * wg) * 32 + lane;
+    const uint32_t lane_off = (uint32_t)(q4 * 32) << 16;
+    const float2 scl2 = make_float2(p.scale_log2, p.scale_log2);
+    const float2 lg2 = make_float2(kLog2e, kLog2e);
+    const uint32_t r7 = (uint32_t)(r & 7) << 4;
+    int qs = 0; uint32_t qph = 0;
+    int ks = 0; uint32_t kph = 0;
+    uint32_t step = 0, bph = 0;
+    for (long long s0 = W.t0; s0 < W.t1; s0 = W.seg_end(s0)) {
+      const long long s1 = W.seg_end(s0);
+      const Unit u = unit_of(s0, p);
+      if (p.dbias2) {  // zero this warpgroup's 32 strip columns of every q-tile
+        uint32_t z[32];
+#pragma unroll
+        for (int k = 0; k < 32; ++k) z[k] = 0u;
+        for (int it = 0; it < p.nQT; ++it) ptx::tmem_st32(tmem + lane_off + kStripCol + it * 64 + wg * 32, z);
+      }
+      if (p.has_bias2) ptx::mbar_wait(bias_full, bph);
+      for (long long a = s0; a < s1; ++a) {
+        // bias1 chunk of this row -> fp32 * log2e (keys >= L masked with -inf)
+        ptx::mbar_wait(&k_full[ks], kph);
+        float* b1f = sB1f + wg * 64 + (ks & 1) * 32;  // per-WG double buffer
+        if (tid_wg < 32) {
+          const int j = u.jt * kBN + wg * 32 + tid_wg;
+          float x = 0.f;
+          if (p.bias1) {
+            const uint16_t raw = sB1[ks * 64 + wg * 32 + tid_wg];
+            x = (F16 ? __half2float(__ushort_as_half(raw)) : __uint_as_float((uint32_t)raw << 16)) * kLog2e;
+          }
+          b1f[tid_wg] = j < p.L ? x : -INFINITY;
+        }
+        ptx::named_bar_sync(1 + wg, 128);
+        const uint32_t b1a = ptx::smem_u32(b1f);
+        for (int it = 0; it < p.nQT; ++it) {
+          const uint32_t sb = step & 1, ph = (step >> 1) & 1;
+          ptx::mbar_wait(&q_full[qs], qph);
+          const float lse2 = ptx::lds_f32(ptx::smem_u32(sLse + qs * kBM + r));
+          const float dl = ptx::lds_f32(ptx::smem_u32(sDel + qs * kBM + r));
+          const float2 nl = make_float2(-lse2, -lse2);
+          const float2 nd = make_float2(-dl, -dl);
+          ptx::mbar_wait(&s_full[sb], ph);
+          ptx::mbar_wait(&pds_free[sb], ph ^ 1);  // P/dS buffer sb: MMAs of step-2 done
+          ptx::tc_fence_after();
+          const uint32_t bt = ptx::smem_u32(sBias + (size_t)it * C::kBiasTile) + r * 128;
+          const uint32_t pbase = ptx::smem_u32(sP + sb * C::kPdsTile) + r * 128;
+          const uint32_t dbase = ptx::smem_u32(sdS + sb * C::kPdsTile) + r * 128;
+          const uint32_t sa = tmem + lane_off + kStripCol + it * 64 + wg * 32;
+#pragma unroll
+          for (int h2 = 0; h2 < 2; ++h2) {  // 16-key halves
+            const int c0 = wg * 32 + h2 * 16;
+            uint32_t sv[16], dp[16], acc[16];
+            ptx::tmem_ld16(tmem + lane_off + sb * 128 + c0, sv);
+            ptx::tmem_ld16(tmem + lane_off + sb * 128 + 64 + c0, dp);
+            if (p.dbias2) {
+              ptx::tmem_st_wait();
+              ptx::tmem_ld16(sa + h2 * 16, acc);
+            }
+            ptx::tmem_ld_wait();
+            if (h2 == 1) {
+              ptx::tc_fence_before();
+              ptx::mbar_arrive(&s_free[sb]);  // S/dP buffer may be recomputed
+            }
+            uint32_t pk[8], dk[8];
+#pragma unroll
+            for (int c = 0; c < 2; ++c) {  // 8-key chunks
+              const int chunk = wg * 4 + h2 * 2 + c;
+              float2 bb[4];
+              const uint4 f0 = lds128(b1a + (h2 * 16 + c * 8) * 4);
+              const uint4 f1 = lds128(b1a + (h2 * 16 + c * 8 + 4) * 4);
+              const float b1v[8] = {__uint_as_float(f0.x), __uint_as_float(f0.y), __uint_as_float(f0.z),
+                                    __uint_as_float(f0.w), __uint_as_float(f1.x), __uint_as_float(f1.y),
+                                    __uint_as_float(f1.z), __uint_as_float(f1.w)};
+              if (p.has_bias2) {
+                const uint4 raw = lds128(bt + ((uint32_t)(chunk << 4) ^ r7));
+                const uint32_t wv[4] = {raw.x, raw.y, raw.z, raw.w};
+#pragma unroll
+                for (int e = 0; e < 4; ++e)
+                  bb[e] = __ffma2_rn(unpack2<F16>(wv[e]), lg2, make_float2(b1v[2 * e], b1v[2 * e + 1]));
+              } else {
+#pragma unroll
+                for (int e = 0; e < 4; ++e) bb[e] = make_float2(b1v[2 * e], b1v[2 * e + 1]);
+              }
+#pragma unroll
+              for (int e = 0; e < 4; ++e) {
+                const int k = c * 8 + 2 * e;
+                float2 x = __ffma2_rn(make_float2(__uint_as_float(sv[k]), __uint_as_float(sv[k + 1])), scl2, bb[e]);
+                x = __fadd2_rn(x, nl);
+                float2 pr;
+                pr.x = ex2(x.x);
+                pr.y = ex2(x.y);
+                const float2 d =
+                    __fmul2_rn(pr, __fadd2_rn(make_float2(__uint_as_float(dp[k]), __uint_as_float(dp[k + 1])), nd));
+                const float2 ac = __fadd2_rn(make_float2(__uint_as_float(acc[k]), __uint_as_float(acc[k + 1])), d);
+                acc[k] = __float_as_uint(ac.x);
+                acc[k + 1] = __float_as_uint(ac.y);
+                pk[k / 2] = F16 ? ptx::pack_f16(pr.x, pr.y) : ptx::pack_bf16(pr.x, pr.y);
+                dk[k / 2] = F16 ? ptx::pack_f16(d.x, d.y) : ptx::pack_bf16(d.x, d.y);
+              }
+              const uint32_t off = (uint32_t)(chunk << 4) ^ r7;
+              sts128(pbase + off, make_uint4(pk[4 * c], pk[4 * c + 1], pk[4 * c + 2], pk[4 * c + 3]));
+              sts128(dbase + off, make_uint4(dk[4 * c], dk[4 * c + 1], dk[4 * c + 2], dk[4 * c + 3]));
+            }
+            if (p.dbias2) ptx::tmem_st16(sa + h2 * 16, acc);  // dBias2 strip += dS (fp32, TMEM)
+          }
+          ptx::fence_proxy_async_smem();
+          ptx::mbar_arrive(&pds_full[sb]);
+          ++step;
+          if (++qs == C::kQStages) { qs = 0; qph ^= 1; }
+        }
+        if (++ks == C::kKStages) { ks = 0; kph ^= 1; }
+      }
+      // ---- unit end: flush the dBias2 strip (fp32 red.add; one partial per CTA and unit)
+      if (p.dbias2) {
+        ptx::tmem_st_wait();
+        const int j0 = u.jt * kBN + wg * 32;
+        for (int it = 0; it < p.nQT; ++it) {
+          const int i = it * kBM + r;
+          uint32_t st[32];
+          ptx::tmem_ld32(tmem + lane_off + kStripCol + it * 64 + wg * 32, st);
+          ptx::tmem_ld_wait();
+          if (i < p.L) {
+            float* dst = p.dbias2 + (((size_t)u.ob * p.H + u.h) * p.L + i) * p.L + j0;
+#pragma unroll
+            for (int k = 0; k < 32; k += 4)
+              if (j0 + k < p.L)
+                red_v4(dst + k, __uint_as_float(st[k]), __uint_as_float(st[k + 1]), __uint_as_float(st[k + 2]),
+                       __uint_as_float(st[k + 3]));
+          }
+        }
+      }
+      if (p.has_bias2) {
+        ptx::named_bar_sync(1 + wg, 128);
+        if (tid_wg == 0) ptx::mbar_arrive(bias_empty);
+        bph ^= 1;
+      }
+    }
+  } else {
+    // ===================================================== epilogue warpgroup: dQ partials, dK/dV
+    const int q4 = warp & 3;
+    const int r = q4 * 32 + lane;
+    const int tid_e = (warp - 10) * 32 + lane;
+    constexpr uint32_t kDqSwzMask = D == 32 ? 7u : D == 16 ? 3u : 1u;  // SW128 / SW64 / SW32
+    const uint32_t lane_off = (uint32_t)(q4 * 32) << 16;
+    uint32_t step = 0, rows = 0;
+    for (long long s0 = W.t0; s0 < W.t1; s0 = W.seg_end(s0)) {
+      const long long s1 = W.seg_end(s0);
+      const Unit u = unit_of(s0, p);
+      int n = u.n0;
+      for (long long a = s0; a < s1; ++a, ++n) {
+        const int b = u.ob * p.N + n;
+        for (int it = 0; it < p.nQT; ++it) {
+          // ---- dQ partial: TMEM -> staging (fp32, row-major) -> TMA reduce-add into dQacc
+          ptx::mbar_wait(dq_full, step & 1);
+          ptx::tc_fence_after();
+          uint32_t v[D];
+#pragma unroll
+          for (int c0 = 0; c0 < D; c0 += 16) ptx::tmem_ld16(tmem + lane_off + kDqCol + c0, *(uint32_t(*)[16])(&v[c0]));
+          ptx::tmem_ld_wait();
+          ptx::tc_fence_before();
+          ptx::mbar_arrive(dq_free);
+          float* stg = sDq + (step & 1) * kBM * D;
+          if (tid_e == 0) ptx::bulk_wait_read<1>();  // staging buffer of step-2 has been read by TMA
+          ptx::named_bar_sync(3, 128);
+          // row r of the staging tile, 16B chunks swizzled like the fp32 dQ tensor map (D*4-byte rows)
+          const uint32_t sa = ptx::smem_u32(stg) + r * (D * 4);
+#pragma unroll
+          for (int c = 0; c < D; c += 4) {
+            const uint32_t off = sa + c * 4;
+            sts128(off ^ (((off >> 7) & kDqSwzMask) << 4), make_uint4(v[c], v[c + 1], v[c + 2], v[c + 3]));
+          }
+          ptx::fence_proxy_async_smem();
+          ptx::named_bar_sync(3, 128);
+          if (tid_e == 0) {
+            ptx::tma_reduce_add_4d(&tmdQ, stg, 0, u.h, it * kBM, b);
+            ptx::bulk_commit();
+          }
+          ++step;
+        }
+        // ---- dK (x scale), dV of this row: lanes 0-15 hold dK rows, 16-31 dV rows of quadrant q4
+        ptx::mbar_wait(kv_done, rows & 1);
+        ptx::tc_fence_after();
+        uint32_t v[D];
+#pragma unroll
+        for (int c0 = 0; c0 < D; c0 += 16) ptx::tmem_ld16(tmem + lane_off + kDkvCol + c0, *(uint32_t(*)[16])(&v[c0]));
+        ptx::tmem_ld_wait();
+        ptx::tc_fence_before();
+        ptx::mbar_arrive(kv_free);
+        ++rows;
+        const int krow = q4 * 16 + (lane & 15);
+        const int j = u.jt * kBN + krow;
+        if (j < p.L) {
+          const bool isk = lane < 16;
+          const float sc = isk ? p.scale : 1.f;
+          uint32_t ow[D / 2];
+#pragma unroll
+          for (int d = 0; d < D; d += 2)
+            ow[d / 2] = F16 ? ptx::pack_f16(__uint_as_float(v[d]) * sc, __uint_as_float(v[d + 1]) * sc)
+                            : ptx::pack_bf16(__uint_as_float(v[d]) * sc, __uint_as_float(v[d + 1]) * sc);
+          uint4* dst = (uint4*)((uint16_t*)(isk ? p.dk : p.dv) + (((size_t)b * p.L + j) * p.H + u.h) * D);
+#pragma unroll
+          for (int q = 0; q < D / 8; ++q) dst[q] = make_uint4(ow[4 * q], ow[4 * q + 1], ow[4 * q + 2], ow[4 * q + 3]);
+        }
+      }
+    }
+    if (tid_e == 0) ptx::bulk_wait<0>();
+  }
+  ptx::tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    ptx::tc_fence_after();
+    ptx::tmem_dealloc(tmem, 512);
+  }
+}
+
+// lse2 / delta padded to whole 128-row tiles: lse2 = lse * log2e (+inf past L), delta (0 past L)
+__global__ void pad_rows_kernel(const float* __restrict__ lse, const float* __restrict__ delta, float* __restrict__ lse2,
+                                float* __restrict__ delta_p, int L, int Lp, long long rows) {
+  const long long n = rows * Lp;
+  for (long long x = blockIdx.x * (long long)blockDim.x + threadIdx.x; x < n; x += (long long)gridDim.x * blockDim.x) {
+    const long long row = x / Lp;
+    const int i = (int)(x - row * Lp);
+    const bool in = i < L;
+    lse2[x] = in ? lse[row * L + i] * kLog2e : INFINITY;
+    delta_p[x] = in ? delta[row * L + i] : 0.f;
+  }
+}
+
+// dQ (bf16/f16) = scale * dQacc (fp32)
+template <typename T>
+__global__ void dq_convert_kernel(const float* __restrict__ acc, T* __restrict__ dq, size_t n, float scale) {
+  for (size_t x = (blockIdx.x * (size_t)blockDim.x + threadIdx.x) * 4; x < n; x += (size_t)gridDim.x * blockDim.x * 4) {
+    const float4 v = *(const float4*)(acc + x);
+    dq[x] = from_f<T>(v.x * scale);
+    dq[x + 1] = from_f<T>(v.y * scale);
+    dq[x + 2] = from_f<T>(v.z * scale);
+    dq[x + 3] = from_f<T>(v.w * scale);
+  }
+}
+
+}  // namespace bk
+}  // namespace tc
+}  // namespace evo

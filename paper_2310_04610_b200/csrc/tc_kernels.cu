@@ -6,6 +6,7 @@
 #include <cstdio>
 #include <mutex>
 
+#include "tc_bwd.cuh"
 #include "tc_fwd.cuh"
 #include "tc_kernels.cuh"
 
@@ -156,6 +157,97 @@ evo_status launch_fwd(const evo_attn_desc* d, const Shape& s, const void* q, con
   return EVO_OK;
 }
 
+// ---------------------------------------------------------------------------------- backward
+struct BwdScratch {
+  size_t dq, lse2, delta, total;
+};
+size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
+BwdScratch bwd_scratch_layout(const evo_attn_desc* d) {
+  BwdScratch w{};
+  const size_t B = (size_t)d->Bo * d->N;
+  const size_t Lp = (size_t)((d->L + bk::kBM - 1) / bk::kBM) * bk::kBM;
+  w.dq = 0;
+  w.lse2 = align256(B * d->L * d->H * d->D * 4);
+  w.delta = w.lse2 + align256(B * d->H * Lp * 4);
+  w.total = w.delta + align256(B * d->H * Lp * 4);
+  return w;
+}
+
+template <int D>
+size_t bwd_smem_bytes(int nQT) {
+  using C = bk::Cfg<D>;
+  size_t b = 1024;
+  b += (size_t)C::kQStages * 2 * C::kTileQ + (size_t)C::kKStages * 2 * C::kTileK + 4 * (size_t)C::kPdsTile;
+  b += (size_t)nQT * C::kBiasTile + 2 * (size_t)bk::kBM * D * 4;
+  b += (size_t)C::kQStages * bk::kBM * 4 * 2 + 128 * 4 + (size_t)C::kKStages * 64 * 2;
+  b += (size_t)(2 * C::kQStages + 2 * C::kKStages + 8 + 6) * 8 + 16;
+  return b;
+}
+
+template <int D, bool F16>
+evo_status launch_bwd(const evo_attn_desc* d, const Shape& s, const void* dout, const void* q, const void* k,
+                      const void* v, const float* lse, const float* delta, void* dq, void* dk, void* dv,
+                      float* dbias2, void* scratch, cudaStream_t st, int* launches, std::string* err) {
+  const CUtensorMapDataType dt = F16 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT16 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16;
+  const BwdScratch w = bwd_scratch_layout(d);
+  char* ws = (char*)scratch;
+  float* dqacc = (float*)(ws + w.dq);
+  float* lse2 = (float*)(ws + w.lse2);
+  float* delta_p = (float*)(ws + w.delta);
+  CUtensorMap tq, tk, tv, tdo, tb, tdq;
+  memset(&tb, 0, sizeof(tb));
+  if (!map_bl_hd(&tq, q, s, bk::kBM, dt, 2, err) || !map_bl_hd(&tk, k, s, bk::kBN, dt, 2, err) ||
+      !map_bl_hd(&tv, v, s, bk::kBN, dt, 2, err) || !map_bl_hd(&tdo, dout, s, bk::kBM, dt, 2, err) ||
+      !map_bl_hd(&tdq, dqacc, s, bk::kBM, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, err))
+    return EVO_ERR_CUDA;
+  if (s.bias2 && !map_bias(&tb, s.bias2, s, (int)d->Bo, dt, err)) return EVO_ERR_CUDA;
+  bk::Params p{};
+  p.B = s.B; p.N = s.N; p.L = s.L; p.H = s.H; p.Bo = (int)d->Bo;
+  p.nQT = (s.L + bk::kBM - 1) / bk::kBM;
+  p.nKT = (s.L + bk::kBN - 1) / bk::kBN;
+  p.total = (long long)p.Bo * p.H * p.nKT * p.N;
+  p.scale = s.scale;
+  p.scale_log2 = s.scale_log2;
+  p.bias1 = s.bias1;
+  p.lse2 = lse2;
+  p.delta = delta_p;
+  p.dk = dk;
+  p.dv = dv;
+  p.dbias2 = dbias2;
+  p.has_bias2 = s.bias2 != nullptr;
+  const size_t smem = bwd_smem_bytes<D>(p.nQT);
+  if (smem > kMaxSmem) {
+    *err = "backward shared-memory budget exceeded";
+    return EVO_ERR_UNSUPPORTED;
+  }
+  const int Lp = p.nQT * bk::kBM;
+  const long long prow = (long long)s.B * s.H;
+  cudaMemsetAsync(dqacc, 0, (size_t)s.B * s.L * s.H * D * 4, st);
+  bk::pad_rows_kernel<<<(unsigned)std::min<long long>((prow * Lp + 255) / 256, 148 * 16), 256, 0, st>>>(
+      lse, delta, lse2, delta_p, s.L, Lp, prow);
+  ++*launches;
+  auto kern = bk::bwd_kernel<D, F16>;
+  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  const int G = sm_count();
+  const long long units = (long long)p.Bo * p.H * p.nKT;
+  long long grid = std::min<long long>(p.total, G);
+  p.aligned = 0;
+  p.split = 1;
+  if (units <= G) {
+    p.split = (int)std::min<long long>(G / units, p.N);
+    p.aligned = 1;
+    grid = units * p.split;
+  }
+  kern<<<(unsigned)grid, bk::kThreads, smem, st>>>(tq, tk, tv, tdo, tb, tdq, p);
+  ++*launches;
+  const size_t n = (size_t)s.B * s.L * s.H * D;
+  using T = typename std::conditional<F16, __half, __nv_bfloat16>::type;
+  bk::dq_convert_kernel<T><<<(unsigned)std::min<size_t>((n / 4 + 255) / 256, 148 * 32), 256, 0, st>>>(dqacc, (T*)dq, n,
+                                                                                                 s.scale);
+  ++*launches;
+  return EVO_OK;
+}
+
 }  // namespace
 
 bool device_supported() {
@@ -174,14 +266,30 @@ bool device_supported() {
 }
 
 size_t fwd_scratch_bytes(const evo_attn_desc*) { return 0; }
-size_t bwd_scratch_bytes(const evo_attn_desc*) { return 0; }
-bool bwd_available(const evo_attn_desc*) { return false; }
+size_t bwd_scratch_bytes(const evo_attn_desc* d) { return bwd_scratch_layout(d).total; }
 
-evo_status bwd(const evo_attn_desc*, const Shape&, const void*, const void*, const void*, const void*,
-               const float*, const float*, void*, void*, void*, float*, float*, void*, cudaStream_t, int*,
-               std::string* err) {
-  *err = "tcgen05 backward not built";
-  return EVO_ERR_UNSUPPORTED;
+// tcgen05 backward: 16-bit inputs, D in {16, 32}, L % 8 == 0 (16B-aligned rows for the bulk copies)
+// and L <= 384 (the dBias2 strip of all query tiles must fit in TMEM next to S/dP, dQ, dK|dV).
+bool bwd_available(const evo_attn_desc* d) {
+  return d->dtype != EVO_F32 && (d->D == 16 || d->D == 32) && d->L % 8 == 0 && d->L <= 3 * bk::kBM &&
+         device_supported();
+}
+
+evo_status bwd(const evo_attn_desc* d, const Shape& s, const void* dout, const void* q, const void* k, const void* v,
+               const float* lse, const float* delta, void* dq, void* dk, void* dv, float* dbias1, float* dbias2,
+               void* scratch, cudaStream_t st, int* launches, std::string* err) {
+  if (dbias1) {
+    *err = "tcgen05 backward does not produce dbias1";
+    return EVO_ERR_UNSUPPORTED;
+  }
+  const bool f16 = d->dtype == EVO_F16;
+  switch (d->D) {
+    case 16: return f16 ? launch_bwd<16, true>(d, s, dout, q, k, v, lse, delta, dq, dk, dv, dbias2, scratch, st, launches, err)
+                        : launch_bwd<16, false>(d, s, dout, q, k, v, lse, delta, dq, dk, dv, dbias2, scratch, st, launches, err);
+    case 32: return f16 ? launch_bwd<32, true>(d, s, dout, q, k, v, lse, delta, dq, dk, dv, dbias2, scratch, st, launches, err)
+                        : launch_bwd<32, false>(d, s, dout, q, k, v, lse, delta, dq, dk, dv, dbias2, scratch, st, launches, err);
+    default: *err = "tcgen05 backward supports D in {16, 32}"; return EVO_ERR_UNSUPPORTED;
+  }
 }
 
 evo_status fwd(const evo_attn_desc* d, const Shape& s, const void* q, const void* k, const void* v, void* o,

@@ -40,17 +40,19 @@ class ShardedStep:
 
 
 def sharded_fwd_bwd(q, k, v, dout, bias1, bias2, group=None, head_chunks: int = 1,
-                    dbias_dtype: torch.dtype = torch.float32) -> ShardedStep:
+                    dbias_dtype: torch.dtype = torch.float32, need_dbias1: bool = False) -> ShardedStep:
     """Forward + backward on this rank's row shard, dBias2 all-reduced.
 
     q/k/v/dout/bias1 are this rank's rows ([Bo, n_local, L, H, D]); bias2 is
     the full pair bias. `head_chunks` > 1 issues the all-reduce per head group
-    on a side stream so it overlaps the next group's compute.
+    on a side stream so it overlaps the next group's compute. The mask-bias
+    gradient is off by default (the MSA mask carries no gradient in OpenFold;
+    the headline step produces dQ, dK, dV and dBias2).
     """
     o, lse = evoformer_attention_forward(q, k, v, bias1, bias2)
     world = dist.get_world_size(group) if dist.is_initialized() else 1
     dq, dk, dv, db1, db2 = evoformer_attention_backward(
-        dout, q, k, v, o, lse, bias1, bias2, need_dbias1=bias1 is not None,
+        dout, q, k, v, o, lse, bias1, bias2, need_dbias1=need_dbias1 and bias1 is not None,
         need_dbias2=bias2 is not None, dbias_dtype=torch.float32)
     if db2 is not None and world > 1:
         dist.all_reduce(db2, op=dist.ReduceOp.SUM, group=group)

@@ -26,6 +26,6 @@ for _ in range(a.iters):
     if a.what in ("fwd", "both"):
         o, lse = E.evoformer_attention_forward(q, k, v, b1, b2, path=a.path)
     if a.what in ("bwd", "both"):
-        E.evoformer_attention_backward(do, q, k, v, o, lse, b1, b2, need_dbias1=True, path=a.path)
+        E.evoformer_attention_backward(do, q, k, v, o, lse, b1, b2, need_dbias1=False, path=a.path)
 torch.cuda.synchronize()
 print("ok", a.config, a.what, E.resolved_path(q, b1, b2, a.path))
