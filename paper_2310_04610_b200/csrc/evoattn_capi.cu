@@ -88,8 +88,8 @@ BwdWs bwd_layout(const evo_attn_desc* d) {
 template <typename T, int DP>
 void simt_fwd(const evo::Shape& s, const void* q, const void* k, const void* v, void* o,
               float* lse, cudaStream_t st) {
-  dim3 grid((s.L + evo::simt::kRows - 1) / evo::simt::kRows, s.H, s.B);
-  evo::simt::fwd_kernel<T, DP><<<grid, evo::simt::kRows, 0, st>>>(
+  dim3 grid((s.L + evo::simt::Tiles<DP>::kRows - 1) / evo::simt::Tiles<DP>::kRows, s.H, s.B);
+  evo::simt::fwd_kernel<T, DP><<<grid, evo::simt::Tiles<DP>::kRows, 0, st>>>(
       s, (const T*)q, (const T*)k, (const T*)v, (T*)o, lse);
   ++g_launches;
 }
@@ -100,7 +100,8 @@ evo_status simt_fwd_dispatch(const evo::Shape& s, const void* q, const void* k, 
   if (s.D <= 8) simt_fwd<T, 8>(s, q, k, v, o, lse, st);
   else if (s.D <= 16) simt_fwd<T, 16>(s, q, k, v, o, lse, st);
   else if (s.D <= 32) simt_fwd<T, 32>(s, q, k, v, o, lse, st);
-  else return fail(EVO_ERR_UNSUPPORTED, "SIMT kernels support D <= 32");
+  else if (s.D <= 64) simt_fwd<T, 64>(s, q, k, v, o, lse, st);
+  else return fail(EVO_ERR_UNSUPPORTED, "SIMT kernels support D <= 64");
   return EVO_OK;
 }
 
@@ -108,11 +109,11 @@ template <typename T, int DP>
 void simt_bwd(const evo::Shape& s, const void* dout, const void* q, const void* k, const void* v,
               const float* lse, const float* delta, void* dq, void* dk, void* dv, float* db1,
               float* db2, cudaStream_t st) {
-  dim3 grid((s.L + evo::simt::kRows - 1) / evo::simt::kRows, s.H, s.B);
-  evo::simt::dkdv_kernel<T, DP><<<grid, evo::simt::kRows, 0, st>>>(
+  dim3 grid((s.L + evo::simt::Tiles<DP>::kRows - 1) / evo::simt::Tiles<DP>::kRows, s.H, s.B);
+  evo::simt::dkdv_kernel<T, DP><<<grid, evo::simt::Tiles<DP>::kRows, 0, st>>>(
       s, (const T*)q, (const T*)k, (const T*)v, (const T*)dout, lse, delta, (T*)dk, (T*)dv, db1,
       db2);
-  evo::simt::dq_kernel<T, DP><<<grid, evo::simt::kRows, 0, st>>>(
+  evo::simt::dq_kernel<T, DP><<<grid, evo::simt::Tiles<DP>::kRows, 0, st>>>(
       s, (const T*)q, (const T*)k, (const T*)v, (const T*)dout, lse, delta, (T*)dq);
   g_launches += 2;
 }
@@ -124,7 +125,8 @@ evo_status simt_bwd_dispatch(const evo::Shape& s, const void* dout, const void* 
   if (s.D <= 8) simt_bwd<T, 8>(s, dout, q, k, v, lse, delta, dq, dk, dv, db1, db2, st);
   else if (s.D <= 16) simt_bwd<T, 16>(s, dout, q, k, v, lse, delta, dq, dk, dv, db1, db2, st);
   else if (s.D <= 32) simt_bwd<T, 32>(s, dout, q, k, v, lse, delta, dq, dk, dv, db1, db2, st);
-  else return fail(EVO_ERR_UNSUPPORTED, "SIMT kernels support D <= 32");
+  else if (s.D <= 64) simt_bwd<T, 64>(s, dout, q, k, v, lse, delta, dq, dk, dv, db1, db2, st);
+  else return fail(EVO_ERR_UNSUPPORTED, "SIMT kernels support D <= 64");
   return EVO_OK;
 }
 
@@ -236,15 +238,16 @@ evo_status evo_attn_bwd(const evo_attn_desc* d, const void* dout, const void* q,
     if (db2) cudaMemsetAsync(db2, 0, n2 * 4, cs);
     if (db1) cudaMemsetAsync(db1, 0, n1 * 4, cs);
   }
-  switch (d->dtype) {
-    case EVO_F32: launch_delta<float>(s, dout, o, delta, cs); break;
-    case EVO_BF16: launch_delta<__nv_bfloat16>(s, dout, o, delta, cs); break;
-    default: launch_delta<__half>(s, dout, o, delta, cs); break;
-  }
   if (path == EVO_PATH_TCGEN05 && evo::tc::bwd_available(d) && !dbias1) {
-    st = evo::tc::bwd(d, s, dout, q, k, v, lse, delta, dq, dk, dv, db1, db2, ws + w.tc, cs,
+    // the tcgen05 preamble computes delta itself
+    st = evo::tc::bwd(d, s, dout, q, k, v, o, lse, nullptr, dq, dk, dv, db1, db2, ws + w.tc, cs,
                       &g_launches, &g_err);
   } else {
+    switch (d->dtype) {
+      case EVO_F32: launch_delta<float>(s, dout, o, delta, cs); break;
+      case EVO_BF16: launch_delta<__nv_bfloat16>(s, dout, o, delta, cs); break;
+      default: launch_delta<__half>(s, dout, o, delta, cs); break;
+    }
     switch (d->dtype) {
       case EVO_F32:
         st = simt_bwd_dispatch<float>(s, dout, q, k, v, lse, delta, dq, dk, dv, db1, db2, cs);

@@ -14,16 +14,22 @@
 namespace evo {
 namespace simt {
 
-constexpr int kRows = 64;  // query (fwd, dQ) or key (dK/dV) rows per CTA, one per thread
-constexpr int kKeyTile = 64;
+// Rows per CTA (one per thread) and staged key tile; halved for D = 64 so the fp32 staging
+// buffers stay inside 48 KB of static shared memory.
+template <int DP>
+struct Tiles {
+  static constexpr int kRows = DP <= 32 ? 64 : 32;  // query (fwd, dQ) or key (dK/dV) rows per CTA
+  static constexpr int kKeyTile = DP <= 32 ? 64 : 32;
+};
 constexpr int kQTile = 32;
 
 // ---------------------------------------------------------------- forward
 template <typename T, int DP>
-__global__ void __launch_bounds__(kRows) fwd_kernel(Shape s, const T* __restrict__ q,
+__global__ void __launch_bounds__(Tiles<DP>::kRows) fwd_kernel(Shape s, const T* __restrict__ q,
                                                     const T* __restrict__ k,
                                                     const T* __restrict__ v, T* __restrict__ o,
                                                     float* __restrict__ lse) {
+  constexpr int kRows = Tiles<DP>::kRows, kKeyTile = Tiles<DP>::kKeyTile;
   __shared__ float ks[kKeyTile][DP + 1];
   __shared__ float vs[kKeyTile][DP + 1];
   __shared__ float b1s[kKeyTile];
@@ -126,10 +132,11 @@ __global__ void delta_kernel(Shape s, const T* __restrict__ dout, const T* __res
 
 // ------------------------------------------- backward: dK, dV, dBias (key side)
 template <typename T, int DP>
-__global__ void __launch_bounds__(kRows) dkdv_kernel(
+__global__ void __launch_bounds__(Tiles<DP>::kRows) dkdv_kernel(
     Shape s, const T* __restrict__ q, const T* __restrict__ k, const T* __restrict__ v,
     const T* __restrict__ dout, const float* __restrict__ lse, const float* __restrict__ delta,
     T* __restrict__ dk, T* __restrict__ dv, float* __restrict__ dbias1, float* __restrict__ dbias2) {
+  constexpr int kRows = Tiles<DP>::kRows;
   __shared__ float kv[2][kRows][DP + 1];
   __shared__ float qs[kQTile][DP];
   __shared__ float dos[kQTile][DP];
@@ -206,10 +213,11 @@ __global__ void __launch_bounds__(kRows) dkdv_kernel(
 
 // ------------------------------------------------- backward: dQ (query side)
 template <typename T, int DP>
-__global__ void __launch_bounds__(kRows) dq_kernel(
+__global__ void __launch_bounds__(Tiles<DP>::kRows) dq_kernel(
     Shape s, const T* __restrict__ q, const T* __restrict__ k, const T* __restrict__ v,
     const T* __restrict__ dout, const float* __restrict__ lse, const float* __restrict__ delta,
     T* __restrict__ dq) {
+  constexpr int kRows = Tiles<DP>::kRows, kKeyTile = Tiles<DP>::kKeyTile;
   __shared__ float ks[kKeyTile][DP];
   __shared__ float vs[kKeyTile][DP];
   __shared__ float b1s[kKeyTile];

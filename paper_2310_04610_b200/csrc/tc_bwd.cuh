@@ -11,8 +11,9 @@
 //  * the dBias2 strip (all queries x 64 keys, fp32) stays in TMEM for the whole unit: every row's
 //    dS is reduced into it on chip (the broadcast-reverse sum of attention_tiled.cpp:318-323 done
 //    in the kernel), and it leaves the SM once, as a fp32 red.add per unit — not once per row;
-//  * S = Q K^T and dP = dO V^T (M=128 queries, N=64 keys) land in double-buffered TMEM tiles;
-//    two softmax warpgroups (32 keys each) rebuild P from LSE in the log2 domain, form
+//  * S = Q K^T + bias1 and dP = dO V^T (M=128 queries, N=64 keys) land in double-buffered TMEM tiles
+//    (bias1 rides along as one extra K=16 step: ones-column x bias1 row, see A_aug/B_aug);
+//    four softmax warpgroups (16 keys each) rebuild P from LSE in the log2 domain, form
 //    dS = P (dP - delta), add dS into the strip, and write P and dS as bf16 into 128B-swizzled
 //    shared tiles that serve both as MN-major (P^T, dS^T) and K-major (dS) UMMA operands;
 //  * dV += P^T dO and dK += dS^T Q accumulate over the query tiles in two M=64 TMEM accumulators
@@ -30,7 +31,15 @@ namespace bk {
 
 constexpr int kBM = 128;   // queries per tile
 constexpr int kBN = 64;    // keys per tile
-constexpr int kThreads = 64 + 256 + 128;  // TMA, MMA, 2 softmax WGs, epilogue WG
+// warps: 0 TMA producer, 1 gradient MMAs, 2 S/dP MMAs, 3..3+4*kSoftWG softmax warpgroups, then the epilogue WG
+constexpr int kSoftWG = 4;                              // softmax warpgroups, 16 keys each
+constexpr int kKeysPerThread = 64 / kSoftWG;
+constexpr int kSoftWarp0 = 3;
+constexpr int kEpiWarp0 = kSoftWarp0 + 4 * kSoftWG;
+constexpr int kThreads = (kEpiWarp0 + 4) * 32;
+constexpr int kSoftThreads = 128 * kSoftWG;
+constexpr uint32_t kEpiBar = 1 + kSoftWG;               // named barrier of the epilogue WG
+constexpr int kAugA = kBM * 32, kAugB = 64 * 32;        // bias1 augmentation tiles (16 bf16 per row)
 constexpr uint32_t kStripCol = 256, kDqCol = 448, kDkvCol = 480;
 
 template <int D>
@@ -58,7 +67,18 @@ struct Params {
   void* dv;
   float* dbias2;        // [Bo, H, L, L] fp32 accumulator or null
   int has_bias2;
+  int aug;             // extra K-step adding bias1 / scale (bias1 present or L % 64 != 0)
+  uint32_t aug_c;      // (c_lo << 16) | c_hi: 16-bit split of 1/scale
+  unsigned long long* trace;  // bring-up timeline of CTA 0 (null in production)
 };
+
+// CTA-0 timeline of steps [kTrFirst, kTrFirst + 64): 8 events x 64 steps (bring-up aid)
+constexpr uint32_t kTrFirst = 100;
+enum BwdTrace { kTbSIssue = 0, kTbSSeen = 1, kTbPds0 = 2, kTbPds1 = 3, kTbGrads = 4, kTbDqSeen = 5, kTbDqOut = 6,
+                kTbQFull = 7, kTbProdQ = 8, kTbKFull = 9, kTbGradsStart = 10, kTbLoopTop = 11 };
+__device__ __forceinline__ void trace(const Params& p, int ev, uint32_t step) {
+  if (p.trace && blockIdx.x == 0 && step - kTrFirst < 64u) p.trace[ev * 64 + (step - kTrFirst)] = clock64();
+}
 
 struct Walker {
   long long t0, t1, N;
@@ -133,10 +153,11 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint8_t* sdS = sP + 2 * C::kPdsTile;                         // [2] dS tiles
   uint8_t* sBias = sdS + 2 * C::kPdsTile;                      // [nQT] bias strip tiles
   float* sDq = (float*)(sBias + (size_t)p.nQT * C::kBiasTile);  // [2] dQ staging (fp32 128 x D)
-  float* sLse = sDq + 2 * kBM * D;                             // [QS][128] lse * log2e (raw fp32 on arrival)
-  float* sDel = sLse + C::kQStages * kBM;                      // [QS][128]
-  float* sB1f = sDel + C::kQStages * kBM;                      // [2 WG][2][32] bias1 * log2e (fp32)
-  uint16_t* sB1 = (uint16_t*)(sB1f + 128);                     // [KS][64] bias1 chunk (raw)
+  uint8_t* sAaug = (uint8_t*)(sDq + 2 * kBM * D);              // 128 x 16 (1/scale split), SW32
+  uint8_t* sBaug = sAaug + kAugA;                              // [KS] 64 x 16 (bias1 per key), SW32
+  float* sLse = (float*)(sBaug + C::kKStages * kAugB);         // [QS][128] lse * log2e
+  float* sDel = sLse + C::kQStages * kBM;                      // [QS][128] delta
+  uint16_t* sB1 = (uint16_t*)(sDel + C::kQStages * kBM);       // [KS][64] bias1 chunk (raw)
   uint64_t* bars = (uint64_t*)(sB1 + C::kKStages * 64);
   uint64_t* q_full = bars;                          // [QS]
   uint64_t* q_empty = q_full + C::kQStages;         // [QS]
@@ -144,14 +165,14 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* k_empty = k_full + C::kKStages;         // [KS]
   uint64_t* s_full = k_empty + C::kKStages;         // [2] S and dP of a step computed
   uint64_t* s_free = s_full + 2;                    // [2] softmax done reading S/dP of a buffer
-  uint64_t* pds_full = s_free + 2;                  // [2] P/dS of a step written (256 arrivals)
+  uint64_t* pds_full = s_free + 2;                  // [2] P/dS of a step written
   uint64_t* pds_free = pds_full + 2;                // [2] MMAs reading that P/dS buffer done
   uint64_t* dq_full = pds_free + 2;                 // [1] dQ partial computed
   uint64_t* dq_free = dq_full + 1;                  // [1] dQ drained from TMEM
   uint64_t* kv_done = dq_free + 1;                  // [1] dK/dV of a row complete
   uint64_t* kv_free = kv_done + 1;                  // [1] dK/dV read out
   uint64_t* bias_full = kv_free + 1;                // [1] bias strip of the unit landed
-  uint64_t* bias_empty = bias_full + 1;             // [1] strip readers done (2 WGs)
+  uint64_t* bias_empty = bias_full + 1;             // [1] strip readers done (one arrival per WG)
   uint32_t* tmem_slot = (uint32_t*)(bias_empty + 1);
 
   const int warp = threadIdx.x / 32;
@@ -164,8 +185,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     for (int s = 0; s < C::kKStages; ++s) { ptx::mbar_init(&k_full[s], 1); ptx::mbar_init(&k_empty[s], 1); }
     for (int s = 0; s < 2; ++s) {
       ptx::mbar_init(&s_full[s], 1);
-      ptx::mbar_init(&s_free[s], 256);
-      ptx::mbar_init(&pds_full[s], 256);
+      ptx::mbar_init(&s_free[s], kSoftThreads);
+      ptx::mbar_init(&pds_full[s], kSoftThreads);
       ptx::mbar_init(&pds_free[s], 1);
     }
     ptx::mbar_init(dq_full, 1);
@@ -173,9 +194,19 @@ __global__ void __launch_bounds__(kThreads, 1)
     ptx::mbar_init(kv_done, 1);
     ptx::mbar_init(kv_free, 128);
     ptx::mbar_init(bias_full, 1);
-    ptx::mbar_init(bias_empty, 2);
+    ptx::mbar_init(bias_empty, kSoftWG);
     ptx::fence_barrier_init();
   }
+  // A_aug: row i = (c_hi, c_lo, 0, ...): one extra K=16 step of S = Q K^T adds (c_hi + c_lo) * B_aug[j][0..1]
+  // = bias1[j] / scale (two-term split of 1/scale, exact to ~2^-16). 16B chunk 0 of a 32B row sits at
+  // chunk position (i >> 2) & 1 under the 32B swizzle.
+  for (int i = threadIdx.x; i < kBM; i += blockDim.x) {
+    const uint32_t c = (uint32_t)((i >> 2) & 1);
+    uint4* row = (uint4*)(sAaug + i * 32);
+    row[c] = make_uint4(p.aug_c, 0u, 0u, 0u);
+    row[c ^ 1] = make_uint4(0u, 0u, 0u, 0u);
+  }
+  ptx::fence_proxy_async_smem();
   if (warp == 1) ptx::tmem_alloc(tmem_slot, 512);
   ptx::tc_fence_before();
   __syncthreads();
@@ -189,23 +220,23 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (p.has_bias2) ptx::tma_prefetch(&tmB2);
       int qs = 0; uint32_t qph = 0;
       int ks = 0; uint32_t kph = 0;
-      uint32_t bph = 0;
+      uint32_t bph = 0, pstep = 0;
       for (long long s0 = W.t0; s0 < W.t1; s0 = W.seg_end(s0)) {
-        const long long s1 = W.seg_end(s0);
+        const int cnt = (int)(W.seg_end(s0) - s0);
         const Unit u = unit_of(s0, p);
         const int plane = u.ob * p.H + u.h;
         if (p.has_bias2) {
-          ptx::mbar_wait(bias_empty, bph ^ 1);
+          ptx::mbar_wait_spin(bias_empty, bph ^ 1);
           ptx::mbar_expect_tx(bias_full, p.nQT * C::kBiasTile);
           for (int it = 0; it < p.nQT; ++it)
             ptx::tma_load_3d(sBias + (size_t)it * C::kBiasTile, &tmB2, bias_full, u.jt * kBN, it * kBM, plane);
           bph ^= 1;
         }
         int n = u.n0;
-        for (long long a = s0; a < s1; ++a, ++n) {
+        for (int a = 0; a < cnt; ++a, ++n) {
           const int b = u.ob * p.N + n;
           // K, V (and the bias1 chunk) of this row's key tile
-          ptx::mbar_wait(&k_empty[ks], kph ^ 1);
+          ptx::mbar_wait_spin(&k_empty[ks], kph ^ 1);
           const int nk = min(kBN, p.L - u.jt * kBN);  // keys of this tile (multiple of 8)
           const uint32_t b1bytes = p.bias1 ? (uint32_t)nk * 2 : 0u;
           ptx::mbar_expect_tx(&k_full[ks], 2 * C::kTileK + b1bytes);
@@ -216,7 +247,8 @@ __global__ void __launch_bounds__(kThreads, 1)
                      &k_full[ks]);
           if (++ks == C::kKStages) { ks = 0; kph ^= 1; }
           for (int it = 0; it < p.nQT; ++it) {
-            ptx::mbar_wait(&q_empty[qs], qph ^ 1);
+            ptx::mbar_wait_spin(&q_empty[qs], qph ^ 1);
+            trace(p, kTbProdQ, pstep++);
             ptx::mbar_expect_tx(&q_full[qs], 2 * C::kTileQ + 2 * kBM * 4);
             ptx::tma_load_4d(sQ + qs * C::kTileQ, &tmQ, &q_full[qs], 0, u.h, it * kBM, b);
             ptx::tma_load_4d(sdO + qs * C::kTileQ, &tmdO, &q_full[qs], 0, u.h, it * kBM, b);
@@ -229,135 +261,170 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
     }
   } else if (warp == 1) {
-    // ===================================================== MMA issuer (converged warp, one elected lane
-    // issues: descriptors stay in uniform registers)
-    const uint32_t idS = ptx::instr_desc(kBM, kBN, F16, false, false);   // S, dP: K-major A, K-major B
+    // ===================================================== gradient MMA issuer (converged warp, one elected
+    // lane issues; descriptors stay in uniform registers). For every (row, q-tile) step t, once P/dS(t)
+    // are in shared memory: dV += P^T dO, dK += dS^T Q (M=64 accumulators), dQ_t = dS K.
     const uint32_t idKV = ptx::instr_desc(64, D, F16, true, true);       // dV, dK: MN-major A and B
     const uint32_t idQ = ptx::instr_desc(kBM, D, F16, false, true);      // dQ: K-major A, MN-major B
-    const uint32_t q0 = ptx::smem_u32(sQ), do0 = ptx::smem_u32(sdO), k0 = ptx::smem_u32(sK), v0 = ptx::smem_u32(sV);
-    const uint32_t p0 = ptx::smem_u32(sP), ds0 = ptx::smem_u32(sdS);
+    // descriptor low words (start >> 4 | LBO >> 4 << 16) of stage 0; stages and K-steps are added
+    constexpr uint32_t kHiMN = ptx::desc_hi(8 * C::kRowBytes, kSw);   // MN-major dO/Q/K as B
+    constexpr uint32_t kHiP = ptx::desc_hi(1024, 2);                  // P, dS tiles (SW128, both majors)
+    constexpr uint32_t kRow16 = C::kRowBytes;                         // 16 rows of 2*D bytes, >> 4
+    const uint32_t q0n = ptx::desc_lo(ptx::smem_u32(sQ), 16 * C::kRowBytes);
+    const uint32_t do0n = ptx::desc_lo(ptx::smem_u32(sdO), 16 * C::kRowBytes);
+    const uint32_t k0n = ptx::desc_lo(ptx::smem_u32(sK), 16 * C::kRowBytes);
+    const uint32_t p0mn = ptx::desc_lo(ptx::smem_u32(sP), 1024), ds0mn = ptx::desc_lo(ptx::smem_u32(sdS), 1024);
+    const uint32_t ds0k = ptx::desc_lo(ptx::smem_u32(sdS), 16);
+    const uint32_t tdKV = tmem + kDkvCol, tdQ = tmem + kDqCol;
+    int qs = 0, ks = 0;
+    uint32_t step = 0, rows = 0;
+    for (long long s0 = W.t0; s0 < W.t1; s0 = W.seg_end(s0)) {
+      const int cnt = (int)(W.seg_end(s0) - s0);
+      for (int a = 0; a < cnt; ++a) {
+        for (int it = 0; it < p.nQT; ++it) {
+          const uint32_t sb = step & 1, ph = (step >> 1) & 1;
+          const bool first = it == 0, last = it == p.nQT - 1;
+          ptx::mbar_wait_spin(&pds_full[sb], ph);
+          if (first) {  // first q-tile of a row overwrites dK/dV: previous row must be read out
+            ptx::mbar_wait_spin(kv_free, (rows & 1) ^ 1);
+            ++rows;
+          }
+          ptx::mbar_wait_spin(dq_free, (step & 1) ^ 1);
+          ptx::tc_fence_after();
+          const uint32_t pA = p0mn + sb * (C::kPdsTile >> 4);
+          const uint32_t dsA = ds0mn + sb * (C::kPdsTile >> 4);
+          const uint32_t dsK = ds0k + sb * (C::kPdsTile >> 4);
+          const uint32_t qB = q0n + qs * (C::kTileQ >> 4);
+          const uint32_t doB = do0n + qs * (C::kTileQ >> 4);
+          const uint32_t kB = k0n + ks * (C::kTileK >> 4);
+          if (ptx::elect_one()) {
+#pragma unroll
+            for (int kk = 0; kk < kBM / 16; ++kk) {  // K = 128 queries: 16 rows per step
+              // A = P^T / dS^T: MN-major SW128 (64 keys wide), 16 query rows = 2 x 8-row atoms (+2048 B)
+              // B = dO / Q: MN-major (D wide), 16 query rows (+16 * 2D B)
+              const uint32_t acc = (!first || kk > 0) ? 1u : 0u;
+              ptx::mma_ss(tdKV + (16u << 16), ptx::desc_make(pA + kk * 128, kHiP),
+                          ptx::desc_make(doB + kk * kRow16, kHiMN), idKV, acc);  // dV (lanes 16-31 of each quadrant)
+              ptx::mma_ss(tdKV, ptx::desc_make(dsA + kk * 128, kHiP), ptx::desc_make(qB + kk * kRow16, kHiMN), idKV,
+                          acc);                                                  // dK (lanes 0-15)
+            }
+#pragma unroll
+            for (int kk = 0; kk < kBN / 16; ++kk)  // dQ = dS K: K = 64 keys (+32 B in the dS rows)
+              ptx::mma_ss(tdQ, ptx::desc_make(dsK + kk * 2, kHiP), ptx::desc_make(kB + kk * kRow16, kHiMN), idQ,
+                          kk > 0);
+            ptx::tc_commit(dq_full);
+            ptx::tc_commit(&pds_free[sb]);
+            ptx::tc_commit(&q_empty[qs]);  // S/dP of this step completed before P/dS existed
+            if (last) {
+              ptx::tc_commit(kv_done);
+              ptx::tc_commit(&k_empty[ks]);
+            }
+            trace(p, kTbGrads, step);
+          }
+          __syncwarp();
+          ++step;
+          if (++qs == C::kQStages) qs = 0;
+        }
+        if (++ks == C::kKStages) ks = 0;
+      }
+    }
+  } else if (warp == 2) {
+    // ===================================================== S / dP issuer (runs up to two steps ahead)
+    const uint32_t idS = ptx::instr_desc(kBM, kBN, F16, false, false);   // S, dP: K-major A, K-major B
+    constexpr uint32_t kHiK = ptx::desc_hi(8 * C::kRowBytes, kSw);
+    constexpr uint32_t kHiAug = ptx::desc_hi(256, 6);                  // 32-byte rows, SW32
+    const uint32_t q0 = ptx::desc_lo(ptx::smem_u32(sQ), 16), do0 = ptx::desc_lo(ptx::smem_u32(sdO), 16);
+    const uint32_t k0 = ptx::desc_lo(ptx::smem_u32(sK), 16), v0 = ptx::desc_lo(ptx::smem_u32(sV), 16);
+    const uint32_t aA = ptx::desc_lo(ptx::smem_u32(sAaug), 16), aB0 = ptx::desc_lo(ptx::smem_u32(sBaug), 16);
     int qs = 0; uint32_t qph = 0;
     int ks = 0; uint32_t kph = 0;
-    uint32_t step = 0;    // (row, q-tile) steps issued: S buffer = step & 1
-    uint32_t rows = 0;    // rows started (kv_free parity)
-    // gradient MMAs of the previous step
-    bool pend = false; uint32_t pstep = 0; int pqs = 0, pks = 0; bool pfirst = false, plast = false;
-    auto issue_grads = [&]() {
-      const uint32_t sb = pstep & 1, ph = (pstep >> 1) & 1;
-      ptx::mbar_wait_spin(&pds_full[sb], ph);
-      if (pfirst) {  // first q-tile of a row overwrites dK/dV: previous row must be read out
-        ptx::mbar_wait_spin(kv_free, (rows & 1) ^ 1);
-        ++rows;
-      }
-      ptx::mbar_wait_spin(dq_free, (pstep & 1) ^ 1);
-      ptx::tc_fence_after();
-      const uint32_t pA = p0 + sb * C::kPdsTile;
-      const uint32_t dsA = ds0 + sb * C::kPdsTile;
-      const uint32_t qB = q0 + pqs * C::kTileQ;
-      const uint32_t doB = do0 + pqs * C::kTileQ;
-      const uint32_t kB = k0 + pks * C::kTileK;
-      if (ptx::elect_one()) {
-#pragma unroll
-        for (int kk = 0; kk < kBM / 16; ++kk) {  // K = 128 queries: 16 rows per step
-          // A = P^T / dS^T: MN-major SW128 (64 keys wide), 16 query rows = 2 x 8-row atoms
-          const uint64_t aP = ptx::smem_desc(pA + kk * 16 * 128, 1024, 1024, 2);
-          const uint64_t aS = ptx::smem_desc(dsA + kk * 16 * 128, 1024, 1024, 2);
-          // B = dO / Q: MN-major (D wide), 16 query rows
-          const uint64_t bdO = ptx::smem_desc(doB + kk * 16 * C::kRowBytes, 16 * C::kRowBytes, 8 * C::kRowBytes, kSw);
-          const uint64_t bQ = ptx::smem_desc(qB + kk * 16 * C::kRowBytes, 16 * C::kRowBytes, 8 * C::kRowBytes, kSw);
-          const uint32_t acc = (!pfirst || kk > 0) ? 1u : 0u;
-          ptx::mma_ss(tmem + kDkvCol + (16u << 16), aP, bdO, idKV, acc);  // dV (lanes 16-31 of each quadrant)
-          ptx::mma_ss(tmem + kDkvCol, aS, bQ, idKV, acc);                 // dK (lanes 0-15)
-        }
-#pragma unroll
-        for (int kk = 0; kk < kBN / 16; ++kk) {  // dQ = dS K: K = 64 keys
-          const uint64_t aS = ptx::smem_desc(dsA + kk * 32, 16, 1024, 2);  // K-major SW128 rows
-          const uint64_t bK = ptx::smem_desc(kB + kk * 16 * C::kRowBytes, 16 * C::kRowBytes, 8 * C::kRowBytes, kSw);
-          ptx::mma_ss(tmem + kDqCol, aS, bK, idQ, kk > 0);
-        }
-        ptx::tc_commit(dq_full);
-        ptx::tc_commit(&pds_free[sb]);
-        ptx::tc_commit(&q_empty[pqs]);
-        if (plast) {
-          ptx::tc_commit(kv_done);
-          ptx::tc_commit(&k_empty[pks]);
-        }
-      }
-      __syncwarp();
-    };
+    uint32_t step = 0;
     for (long long s0 = W.t0; s0 < W.t1; s0 = W.seg_end(s0)) {
-      const long long s1 = W.seg_end(s0);
-      for (long long a = s0; a < s1; ++a) {
+      const int cnt = (int)(W.seg_end(s0) - s0);
+      const Unit u = unit_of(s0, p);
+      for (int a = 0; a < cnt; ++a) {
         ptx::mbar_wait_spin(&k_full[ks], kph);
-        const uint32_t kA = k0 + ks * C::kTileK;
-        const uint32_t vA = v0 + ks * C::kTileK;
+        if (p.aug) {
+          // B_aug row j = (b1[j], b1[j] or 0 if non-finite) for keys < L, (-inf, 0) past L; 2 rows per lane
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const int jj = lane + 32 * h;
+            const bool in = u.jt * kBN + jj < p.L;
+            uint32_t v0b = 0u, v1b = 0u;
+            if (!in) {
+              v0b = F16 ? 0xFC00u : 0xFF80u;
+            } else if (p.bias1) {
+              v0b = sB1[ks * 64 + jj];
+              const bool fin = F16 ? (v0b & 0x7C00u) != 0x7C00u : (v0b & 0x7F80u) != 0x7F80u;
+              v1b = fin ? v0b : 0u;
+            }
+            const uint32_t c = (uint32_t)((jj >> 2) & 1);
+            uint4* row = (uint4*)(sBaug + ks * kAugB + jj * 32);
+            row[c] = make_uint4(v0b | (v1b << 16), 0u, 0u, 0u);
+            row[c ^ 1] = make_uint4(0u, 0u, 0u, 0u);
+          }
+          ptx::fence_proxy_async_smem();
+          __syncwarp();
+        }
+        if (lane == 0) trace(p, kTbKFull, step);
+        const uint32_t kA = k0 + ks * (C::kTileK >> 4);
+        const uint32_t vA = v0 + ks * (C::kTileK >> 4);
+        const uint32_t bA = aB0 + ks * (kAugB >> 4);
         for (int it = 0; it < p.nQT; ++it) {
           const uint32_t sb = step & 1;
           ptx::mbar_wait_spin(&q_full[qs], qph);
+          if (lane == 0) trace(p, kTbQFull, step);
           ptx::mbar_wait_spin(&s_free[sb], ((step >> 1) & 1) ^ 1);
           ptx::tc_fence_after();
-          const uint32_t qA = q0 + qs * C::kTileQ;
-          const uint32_t doA = do0 + qs * C::kTileQ;
+          const uint32_t qA = q0 + qs * (C::kTileQ >> 4);
+          const uint32_t doA = do0 + qs * (C::kTileQ >> 4);
           if (ptx::elect_one()) {
 #pragma unroll
-            for (int kk = 0; kk < D / 16; ++kk) {
-              const uint64_t a1 = ptx::smem_desc(qA + kk * 32, 16, 8 * C::kRowBytes, kSw);
-              const uint64_t b1 = ptx::smem_desc(kA + kk * 32, 16, 8 * C::kRowBytes, kSw);
-              ptx::mma_ss(tmem + sb * 128, a1, b1, idS, kk > 0);          // S
-              const uint64_t a2 = ptx::smem_desc(doA + kk * 32, 16, 8 * C::kRowBytes, kSw);
-              const uint64_t b2 = ptx::smem_desc(vA + kk * 32, 16, 8 * C::kRowBytes, kSw);
-              ptx::mma_ss(tmem + sb * 128 + 64, a2, b2, idS, kk > 0);     // dP
+            for (int kk = 0; kk < D / 16; ++kk) {  // +32 B along the K-major rows
+              ptx::mma_ss(tmem + sb * 128, ptx::desc_make(qA + kk * 2, kHiK), ptx::desc_make(kA + kk * 2, kHiK), idS,
+                          kk > 0);  // S
+              ptx::mma_ss(tmem + sb * 128 + 64, ptx::desc_make(doA + kk * 2, kHiK), ptx::desc_make(vA + kk * 2, kHiK),
+                          idS, kk > 0);  // dP
             }
+            if (p.aug) ptx::mma_ss(tmem + sb * 128, ptx::desc_make(aA, kHiAug), ptx::desc_make(bA, kHiAug), idS, 1u);
             ptx::tc_commit(&s_full[sb]);
+            trace(p, kTbSIssue, step);
           }
           __syncwarp();
-          if (pend) issue_grads();
-          pend = true; pstep = step; pqs = qs; pks = ks; pfirst = (it == 0); plast = (it == p.nQT - 1);
+          if (p.trace && blockIdx.x == 0 && step - kTrFirst < 64u) {  // bring-up: S completion time
+            ptx::mbar_wait_spin(&s_full[sb], (step >> 1) & 1);
+            if (lane == 0) trace(p, kTbLoopTop, step);
+          }
           ++step;
           if (++qs == C::kQStages) { qs = 0; qph ^= 1; }
         }
         if (++ks == C::kKStages) { ks = 0; kph ^= 1; }
       }
     }
-    if (pend) issue_grads();
-  } else if (warp < 10) {
-    // ===================================================== softmax warpgroups (2 x 32 keys)
-    const int wg = (warp - 2) / 4;
+  } else if (warp < kEpiWarp0) {
+    // ===================================================== softmax warpgroups (kSoftWG x 16 keys)
+    const int wg = (warp - kSoftWarp0) / 4;
     const int q4 = warp & 3;
     const int r = q4 * 32 + lane;                 // query row in tile == TMEM lane
-    const int tid_wg = (warp - 2 - 4 * wg) * 32 + lane;
+    const int tid_wg = (warp - kSoftWarp0 - 4 * wg) * 32 + lane;
     const uint32_t lane_off = (uint32_t)(q4 * 32) << 16;
+    const uint32_t col = (uint32_t)(wg * kKeysPerThread);
     const float2 scl2 = make_float2(p.scale_log2, p.scale_log2);
     const float2 lg2 = make_float2(kLog2e, kLog2e);
     const uint32_t r7 = (uint32_t)(r & 7) << 4;
     int qs = 0; uint32_t qph = 0;
-    int ks = 0; uint32_t kph = 0;
     uint32_t step = 0, bph = 0;
     for (long long s0 = W.t0; s0 < W.t1; s0 = W.seg_end(s0)) {
-      const long long s1 = W.seg_end(s0);
+      const int cnt = (int)(W.seg_end(s0) - s0);
       const Unit u = unit_of(s0, p);
-      if (p.dbias2) {  // zero this warpgroup's 32 strip columns of every q-tile
-        uint32_t z[32];
+      if (p.dbias2) {  // zero this thread's strip columns of every q-tile
+        uint32_t z[16];
 #pragma unroll
-        for (int k = 0; k < 32; ++k) z[k] = 0u;
-        for (int it = 0; it < p.nQT; ++it) ptx::tmem_st32(tmem + lane_off + kStripCol + it * 64 + wg * 32, z);
+        for (int k = 0; k < 16; ++k) z[k] = 0u;
+        for (int it = 0; it < p.nQT; ++it) ptx::tmem_st16(tmem + lane_off + kStripCol + it * 64 + col, z);
       }
       if (p.has_bias2) ptx::mbar_wait(bias_full, bph);
-      for (long long a = s0; a < s1; ++a) {
-        // bias1 chunk of this row -> fp32 * log2e (keys >= L masked with -inf)
-        ptx::mbar_wait(&k_full[ks], kph);
-        float* b1f = sB1f + wg * 64 + (ks & 1) * 32;  // per-WG double buffer
-        if (tid_wg < 32) {
-          const int j = u.jt * kBN + wg * 32 + tid_wg;
-          float x = 0.f;
-          if (p.bias1) {
-            const uint16_t raw = sB1[ks * 64 + wg * 32 + tid_wg];
-            x = (F16 ? __half2float(__ushort_as_half(raw)) : __uint_as_float((uint32_t)raw << 16)) * kLog2e;
-          }
-          b1f[tid_wg] = j < p.L ? x : -INFINITY;
-        }
-        ptx::named_bar_sync(1 + wg, 128);
-        const uint32_t b1a = ptx::smem_u32(b1f);
+      for (int a = 0; a < cnt; ++a) {
         for (int it = 0; it < p.nQT; ++it) {
           const uint32_t sb = step & 1, ph = (step >> 1) & 1;
           ptx::mbar_wait(&q_full[qs], qph);
@@ -366,89 +433,78 @@ __global__ void __launch_bounds__(kThreads, 1)
           const float2 nl = make_float2(-lse2, -lse2);
           const float2 nd = make_float2(-dl, -dl);
           ptx::mbar_wait(&s_full[sb], ph);
+          if (tid_wg == 0 && wg == 0) trace(p, kTbSSeen, step);
           ptx::mbar_wait(&pds_free[sb], ph ^ 1);  // P/dS buffer sb: MMAs of step-2 done
           ptx::tc_fence_after();
+          // all loads of the step in flight together: S, dP, the strip (TMEM) and the bias2 row (smem)
+          const uint32_t sa = tmem + lane_off + kStripCol + it * 64 + col;
+          uint32_t sv[16], dp[16], acc[16];
+          ptx::tmem_ld16(tmem + lane_off + sb * 128 + col, sv);
+          ptx::tmem_ld16(tmem + lane_off + sb * 128 + 64 + col, dp);
+          if (p.dbias2) {
+            ptx::tmem_st_wait();
+            ptx::tmem_ld16(sa, acc);
+          }
+          uint4 braw[2] = {make_uint4(0u, 0u, 0u, 0u), make_uint4(0u, 0u, 0u, 0u)};
           const uint32_t bt = ptx::smem_u32(sBias + (size_t)it * C::kBiasTile) + r * 128;
+          if (p.has_bias2) {
+            braw[0] = lds128(bt + ((uint32_t)((2 * wg) << 4) ^ r7));
+            braw[1] = lds128(bt + ((uint32_t)((2 * wg + 1) << 4) ^ r7));
+          }
+          ptx::tmem_ld_wait();
+          ptx::tc_fence_before();
+          ptx::mbar_arrive(&s_free[sb]);  // S/dP buffer may be recomputed
+          uint32_t pk[8], dk[8];
+#pragma unroll
+          for (int c = 0; c < 2; ++c) {
+            const uint32_t wv[4] = {braw[c].x, braw[c].y, braw[c].z, braw[c].w};
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              const int k = c * 8 + 2 * e;
+              const float2 bb = __ffma2_rn(unpack2<F16>(wv[e]), lg2, nl);  // bias2 * log2e - lse * log2e
+              const float2 x = __ffma2_rn(make_float2(__uint_as_float(sv[k]), __uint_as_float(sv[k + 1])), scl2, bb);
+              float2 pr;
+              pr.x = ex2(x.x);
+              pr.y = ex2(x.y);
+              const float2 d =
+                  __fmul2_rn(pr, __fadd2_rn(make_float2(__uint_as_float(dp[k]), __uint_as_float(dp[k + 1])), nd));
+              const float2 ac = __fadd2_rn(make_float2(__uint_as_float(acc[k]), __uint_as_float(acc[k + 1])), d);
+              acc[k] = __float_as_uint(ac.x);
+              acc[k + 1] = __float_as_uint(ac.y);
+              pk[k / 2] = F16 ? ptx::pack_f16(pr.x, pr.y) : ptx::pack_bf16(pr.x, pr.y);
+              dk[k / 2] = F16 ? ptx::pack_f16(d.x, d.y) : ptx::pack_bf16(d.x, d.y);
+            }
+          }
+          // P and dS -> shared (128B swizzle; chunks 2wg, 2wg+1 of row r)
           const uint32_t pbase = ptx::smem_u32(sP + sb * C::kPdsTile) + r * 128;
           const uint32_t dbase = ptx::smem_u32(sdS + sb * C::kPdsTile) + r * 128;
-          const uint32_t sa = tmem + lane_off + kStripCol + it * 64 + wg * 32;
 #pragma unroll
-          for (int h2 = 0; h2 < 2; ++h2) {  // 16-key halves
-            const int c0 = wg * 32 + h2 * 16;
-            uint32_t sv[16], dp[16], acc[16];
-            ptx::tmem_ld16(tmem + lane_off + sb * 128 + c0, sv);
-            ptx::tmem_ld16(tmem + lane_off + sb * 128 + 64 + c0, dp);
-            if (p.dbias2) {
-              ptx::tmem_st_wait();
-              ptx::tmem_ld16(sa + h2 * 16, acc);
-            }
-            ptx::tmem_ld_wait();
-            if (h2 == 1) {
-              ptx::tc_fence_before();
-              ptx::mbar_arrive(&s_free[sb]);  // S/dP buffer may be recomputed
-            }
-            uint32_t pk[8], dk[8];
-#pragma unroll
-            for (int c = 0; c < 2; ++c) {  // 8-key chunks
-              const int chunk = wg * 4 + h2 * 2 + c;
-              float2 bb[4];
-              const uint4 f0 = lds128(b1a + (h2 * 16 + c * 8) * 4);
-              const uint4 f1 = lds128(b1a + (h2 * 16 + c * 8 + 4) * 4);
-              const float b1v[8] = {__uint_as_float(f0.x), __uint_as_float(f0.y), __uint_as_float(f0.z),
-                                    __uint_as_float(f0.w), __uint_as_float(f1.x), __uint_as_float(f1.y),
-                                    __uint_as_float(f1.z), __uint_as_float(f1.w)};
-              if (p.has_bias2) {
-                const uint4 raw = lds128(bt + ((uint32_t)(chunk << 4) ^ r7));
-                const uint32_t wv[4] = {raw.x, raw.y, raw.z, raw.w};
-#pragma unroll
-                for (int e = 0; e < 4; ++e)
-                  bb[e] = __ffma2_rn(unpack2<F16>(wv[e]), lg2, make_float2(b1v[2 * e], b1v[2 * e + 1]));
-              } else {
-#pragma unroll
-                for (int e = 0; e < 4; ++e) bb[e] = make_float2(b1v[2 * e], b1v[2 * e + 1]);
-              }
-#pragma unroll
-              for (int e = 0; e < 4; ++e) {
-                const int k = c * 8 + 2 * e;
-                float2 x = __ffma2_rn(make_float2(__uint_as_float(sv[k]), __uint_as_float(sv[k + 1])), scl2, bb[e]);
-                x = __fadd2_rn(x, nl);
-                float2 pr;
-                pr.x = ex2(x.x);
-                pr.y = ex2(x.y);
-                const float2 d =
-                    __fmul2_rn(pr, __fadd2_rn(make_float2(__uint_as_float(dp[k]), __uint_as_float(dp[k + 1])), nd));
-                const float2 ac = __fadd2_rn(make_float2(__uint_as_float(acc[k]), __uint_as_float(acc[k + 1])), d);
-                acc[k] = __float_as_uint(ac.x);
-                acc[k + 1] = __float_as_uint(ac.y);
-                pk[k / 2] = F16 ? ptx::pack_f16(pr.x, pr.y) : ptx::pack_bf16(pr.x, pr.y);
-                dk[k / 2] = F16 ? ptx::pack_f16(d.x, d.y) : ptx::pack_bf16(d.x, d.y);
-              }
-              const uint32_t off = (uint32_t)(chunk << 4) ^ r7;
-              sts128(pbase + off, make_uint4(pk[4 * c], pk[4 * c + 1], pk[4 * c + 2], pk[4 * c + 3]));
-              sts128(dbase + off, make_uint4(dk[4 * c], dk[4 * c + 1], dk[4 * c + 2], dk[4 * c + 3]));
-            }
-            if (p.dbias2) ptx::tmem_st16(sa + h2 * 16, acc);  // dBias2 strip += dS (fp32, TMEM)
+          for (int c = 0; c < 2; ++c) {
+            const uint32_t off = (uint32_t)((2 * wg + c) << 4) ^ r7;
+            sts128(pbase + off, make_uint4(pk[4 * c], pk[4 * c + 1], pk[4 * c + 2], pk[4 * c + 3]));
+            sts128(dbase + off, make_uint4(dk[4 * c], dk[4 * c + 1], dk[4 * c + 2], dk[4 * c + 3]));
           }
           ptx::fence_proxy_async_smem();
           ptx::mbar_arrive(&pds_full[sb]);
+          if (tid_wg == 0) trace(p, wg == 0 ? kTbPds0 : kTbPds1, step);
+          if (p.dbias2) ptx::tmem_st16(sa, acc);  // dBias2 strip += dS (fp32, TMEM)
           ++step;
           if (++qs == C::kQStages) { qs = 0; qph ^= 1; }
         }
-        if (++ks == C::kKStages) { ks = 0; kph ^= 1; }
       }
       // ---- unit end: flush the dBias2 strip (fp32 red.add; one partial per CTA and unit)
       if (p.dbias2) {
         ptx::tmem_st_wait();
-        const int j0 = u.jt * kBN + wg * 32;
+        const int j0 = u.jt * kBN + (int)col;
         for (int it = 0; it < p.nQT; ++it) {
           const int i = it * kBM + r;
-          uint32_t st[32];
-          ptx::tmem_ld32(tmem + lane_off + kStripCol + it * 64 + wg * 32, st);
+          uint32_t st[16];
+          ptx::tmem_ld16(tmem + lane_off + kStripCol + it * 64 + col, st);
           ptx::tmem_ld_wait();
           if (i < p.L) {
             float* dst = p.dbias2 + (((size_t)u.ob * p.H + u.h) * p.L + i) * p.L + j0;
 #pragma unroll
-            for (int k = 0; k < 32; k += 4)
+            for (int k = 0; k < 16; k += 4)
               if (j0 + k < p.L)
                 red_v4(dst + k, __uint_as_float(st[k]), __uint_as_float(st[k + 1]), __uint_as_float(st[k + 2]),
                        __uint_as_float(st[k + 3]));
@@ -465,19 +521,20 @@ __global__ void __launch_bounds__(kThreads, 1)
     // ===================================================== epilogue warpgroup: dQ partials, dK/dV
     const int q4 = warp & 3;
     const int r = q4 * 32 + lane;
-    const int tid_e = (warp - 10) * 32 + lane;
+    const int tid_e = (warp - kEpiWarp0) * 32 + lane;
     constexpr uint32_t kDqSwzMask = D == 32 ? 7u : D == 16 ? 3u : 1u;  // SW128 / SW64 / SW32
     const uint32_t lane_off = (uint32_t)(q4 * 32) << 16;
     uint32_t step = 0, rows = 0;
     for (long long s0 = W.t0; s0 < W.t1; s0 = W.seg_end(s0)) {
-      const long long s1 = W.seg_end(s0);
+      const int cnt = (int)(W.seg_end(s0) - s0);
       const Unit u = unit_of(s0, p);
       int n = u.n0;
-      for (long long a = s0; a < s1; ++a, ++n) {
+      for (int a = 0; a < cnt; ++a, ++n) {
         const int b = u.ob * p.N + n;
         for (int it = 0; it < p.nQT; ++it) {
-          // ---- dQ partial: TMEM -> staging (fp32, row-major) -> TMA reduce-add into dQacc
+          // ---- dQ partial: TMEM -> staging (fp32, swizzled rows) -> TMA reduce-add into dQacc
           ptx::mbar_wait(dq_full, step & 1);
+          if (tid_e == 0) trace(p, kTbDqSeen, step);
           ptx::tc_fence_after();
           uint32_t v[D];
 #pragma unroll
@@ -487,7 +544,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           ptx::mbar_arrive(dq_free);
           float* stg = sDq + (step & 1) * kBM * D;
           if (tid_e == 0) ptx::bulk_wait_read<1>();  // staging buffer of step-2 has been read by TMA
-          ptx::named_bar_sync(3, 128);
+          ptx::named_bar_sync(kEpiBar, 128);
           // row r of the staging tile, 16B chunks swizzled like the fp32 dQ tensor map (D*4-byte rows)
           const uint32_t sa = ptx::smem_u32(stg) + r * (D * 4);
 #pragma unroll
@@ -496,10 +553,11 @@ __global__ void __launch_bounds__(kThreads, 1)
             sts128(off ^ (((off >> 7) & kDqSwzMask) << 4), make_uint4(v[c], v[c + 1], v[c + 2], v[c + 3]));
           }
           ptx::fence_proxy_async_smem();
-          ptx::named_bar_sync(3, 128);
+          ptx::named_bar_sync(kEpiBar, 128);
           if (tid_e == 0) {
             ptx::tma_reduce_add_4d(&tmdQ, stg, 0, u.h, it * kBM, b);
             ptx::bulk_commit();
+            trace(p, kTbDqOut, step);
           }
           ++step;
         }
@@ -536,6 +594,40 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (warp == 1) {
     ptx::tc_fence_after();
     ptx::tmem_dealloc(tmem, 512);
+  }
+}
+
+// Backward preamble (one pass over dO and O): delta[b,h,i] = sum_d dO*O (attention_tiled.cpp:254-262)
+// and lse2 = lse * log2e, both laid out [B, H, Lp] with the rows past L padded (+inf / 0).
+// Thread per (b, i, h): D contiguous elements of dO and O, 16-byte loads.
+template <int D, typename T>
+__global__ void prep_kernel(const T* __restrict__ dout, const T* __restrict__ o, const float* __restrict__ lse,
+                            float* __restrict__ lse2, float* __restrict__ delta_p, int B, int L, int H, int Lp) {
+  const long long n = (long long)B * Lp * H;
+  for (long long x = blockIdx.x * (long long)blockDim.x + threadIdx.x; x < n; x += (long long)gridDim.x * blockDim.x) {
+    const int h = (int)(x % H);
+    const long long bi = x / H;
+    const int i = (int)(bi % Lp);
+    const int b = (int)(bi / Lp);
+    const size_t orow = ((size_t)b * H + h) * Lp + i;
+    if (i >= L) {
+      lse2[orow] = INFINITY;
+      delta_p[orow] = 0.f;
+      continue;
+    }
+    const uint4* a4 = (const uint4*)(dout + (((size_t)b * L + i) * H + h) * D);
+    const uint4* b4 = (const uint4*)(o + (((size_t)b * L + i) * H + h) * D);
+    float acc = 0.f;
+#pragma unroll
+    for (int c = 0; c < D / 8; ++c) {
+      const uint4 u = __ldg(a4 + c), w = __ldg(b4 + c);
+      const T* ue = (const T*)&u;
+      const T* we = (const T*)&w;
+#pragma unroll
+      for (int e = 0; e < 8; ++e) acc = fmaf(to_f(ue[e]), to_f(we[e]), acc);
+    }
+    delta_p[orow] = acc;
+    lse2[orow] = lse[((size_t)b * H + h) * L + i] * kLog2e;
   }
 }
 

@@ -4,6 +4,7 @@
 #include <cudaTypedefs.h>
 
 #include <cstdio>
+#include <cstdlib>
 #include <mutex>
 
 #include "tc_bwd.cuh"
@@ -14,6 +15,7 @@ namespace evo {
 namespace tc {
 
 unsigned long long* g_trace = nullptr;
+unsigned long long* g_trace_bwd = nullptr;
 
 namespace {
 
@@ -179,14 +181,15 @@ size_t bwd_smem_bytes(int nQT) {
   size_t b = 1024;
   b += (size_t)C::kQStages * 2 * C::kTileQ + (size_t)C::kKStages * 2 * C::kTileK + 4 * (size_t)C::kPdsTile;
   b += (size_t)nQT * C::kBiasTile + 2 * (size_t)bk::kBM * D * 4;
-  b += (size_t)C::kQStages * bk::kBM * 4 * 2 + 128 * 4 + (size_t)C::kKStages * 64 * 2;
+  b += (size_t)bk::kAugA + (size_t)C::kKStages * bk::kAugB;
+  b += (size_t)C::kQStages * bk::kBM * 4 * 2 + (size_t)C::kKStages * 64 * 2;
   b += (size_t)(2 * C::kQStages + 2 * C::kKStages + 8 + 6) * 8 + 16;
   return b;
 }
 
 template <int D, bool F16>
 evo_status launch_bwd(const evo_attn_desc* d, const Shape& s, const void* dout, const void* q, const void* k,
-                      const void* v, const float* lse, const float* delta, void* dq, void* dk, void* dv,
+                      const void* v, const void* o, const float* lse, const float* delta, void* dq, void* dk, void* dv,
                       float* dbias2, void* scratch, cudaStream_t st, int* launches, std::string* err) {
   const CUtensorMapDataType dt = F16 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT16 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16;
   const BwdScratch w = bwd_scratch_layout(d);
@@ -215,6 +218,26 @@ evo_status launch_bwd(const evo_attn_desc* d, const Shape& s, const void* dout, 
   p.dv = dv;
   p.dbias2 = dbias2;
   p.has_bias2 = s.bias2 != nullptr;
+  p.trace = g_trace_bwd;
+  // bias1 (and the key mask past L) enter S through one extra K=16 MMA step: A_aug rows hold a
+  // 16-bit two-term split of 1/scale, B_aug rows the bias1 value of each key.
+  p.aug = (s.bias1 != nullptr || s.L % bk::kBN != 0) ? 1 : 0;
+  {
+    const double c = 1.0 / (double)s.scale;
+    uint16_t hi, lo;
+    if (F16) {
+      const __half h = __double2half(c);
+      const __half l = __double2half(c - (double)__half2float(h));
+      hi = *(const uint16_t*)&h;
+      lo = *(const uint16_t*)&l;
+    } else {
+      const __nv_bfloat16 h = __double2bfloat16(c);
+      const __nv_bfloat16 l = __double2bfloat16(c - (double)__bfloat162float(h));
+      hi = *(const uint16_t*)&h;
+      lo = *(const uint16_t*)&l;
+    }
+    p.aug_c = (uint32_t)hi | ((uint32_t)lo << 16);
+  }
   const size_t smem = bwd_smem_bytes<D>(p.nQT);
   if (smem > kMaxSmem) {
     *err = "backward shared-memory budget exceeded";
@@ -223,8 +246,14 @@ evo_status launch_bwd(const evo_attn_desc* d, const Shape& s, const void* dout, 
   const int Lp = p.nQT * bk::kBM;
   const long long prow = (long long)s.B * s.H;
   cudaMemsetAsync(dqacc, 0, (size_t)s.B * s.L * s.H * D * 4, st);
-  bk::pad_rows_kernel<<<(unsigned)std::min<long long>((prow * Lp + 255) / 256, 148 * 16), 256, 0, st>>>(
-      lse, delta, lse2, delta_p, s.L, Lp, prow);
+  using T = typename std::conditional<F16, __half, __nv_bfloat16>::type;
+  if (delta) {  // delta supplied by the caller: only pad
+    bk::pad_rows_kernel<<<(unsigned)std::min<long long>((prow * Lp + 255) / 256, 148 * 16), 256, 0, st>>>(
+        lse, delta, lse2, delta_p, s.L, Lp, prow);
+  } else {
+    bk::prep_kernel<D, T><<<(unsigned)std::min<long long>((prow * Lp + 255) / 256, 148 * 32), 256, 0, st>>>(
+        (const T*)dout, (const T*)o, lse, lse2, delta_p, s.B, s.L, s.H, Lp);
+  }
   ++*launches;
   auto kern = bk::bwd_kernel<D, F16>;
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -241,7 +270,6 @@ evo_status launch_bwd(const evo_attn_desc* d, const Shape& s, const void* dout, 
   kern<<<(unsigned)grid, bk::kThreads, smem, st>>>(tq, tk, tv, tdo, tb, tdq, p);
   ++*launches;
   const size_t n = (size_t)s.B * s.L * s.H * D;
-  using T = typename std::conditional<F16, __half, __nv_bfloat16>::type;
   bk::dq_convert_kernel<T><<<(unsigned)std::min<size_t>((n / 4 + 255) / 256, 148 * 32), 256, 0, st>>>(dqacc, (T*)dq, n,
                                                                                                  s.scale);
   ++*launches;
@@ -276,7 +304,7 @@ bool bwd_available(const evo_attn_desc* d) {
 }
 
 evo_status bwd(const evo_attn_desc* d, const Shape& s, const void* dout, const void* q, const void* k, const void* v,
-               const float* lse, const float* delta, void* dq, void* dk, void* dv, float* dbias1, float* dbias2,
+               const void* o, const float* lse, const float* delta, void* dq, void* dk, void* dv, float* dbias1, float* dbias2,
                void* scratch, cudaStream_t st, int* launches, std::string* err) {
   if (dbias1) {
     *err = "tcgen05 backward does not produce dbias1";
@@ -284,10 +312,10 @@ evo_status bwd(const evo_attn_desc* d, const Shape& s, const void* dout, const v
   }
   const bool f16 = d->dtype == EVO_F16;
   switch (d->D) {
-    case 16: return f16 ? launch_bwd<16, true>(d, s, dout, q, k, v, lse, delta, dq, dk, dv, dbias2, scratch, st, launches, err)
-                        : launch_bwd<16, false>(d, s, dout, q, k, v, lse, delta, dq, dk, dv, dbias2, scratch, st, launches, err);
-    case 32: return f16 ? launch_bwd<32, true>(d, s, dout, q, k, v, lse, delta, dq, dk, dv, dbias2, scratch, st, launches, err)
-                        : launch_bwd<32, false>(d, s, dout, q, k, v, lse, delta, dq, dk, dv, dbias2, scratch, st, launches, err);
+    case 16: return f16 ? launch_bwd<16, true>(d, s, dout, q, k, v, o, lse, delta, dq, dk, dv, dbias2, scratch, st, launches, err)
+                        : launch_bwd<16, false>(d, s, dout, q, k, v, o, lse, delta, dq, dk, dv, dbias2, scratch, st, launches, err);
+    case 32: return f16 ? launch_bwd<32, true>(d, s, dout, q, k, v, o, lse, delta, dq, dk, dv, dbias2, scratch, st, launches, err)
+                        : launch_bwd<32, false>(d, s, dout, q, k, v, o, lse, delta, dq, dk, dv, dbias2, scratch, st, launches, err);
     default: *err = "tcgen05 backward supports D in {16, 32}"; return EVO_ERR_UNSUPPORTED;
   }
 }
@@ -312,3 +340,4 @@ evo_status fwd(const evo_attn_desc* d, const Shape& s, const void* q, const void
 // Bring-up aid (not part of include/evoattn.h): record a clock64 timeline of CTA 0 of the next
 // forward launches into a device buffer of 8 x 64 uint64 (null disables).
 extern "C" void evo_attn_debug_set_trace(void* dev_buf) { evo::tc::g_trace = (unsigned long long*)dev_buf; }
+extern "C" void evo_attn_debug_set_trace_bwd(void* dev_buf) { evo::tc::g_trace_bwd = (unsigned long long*)dev_buf; }

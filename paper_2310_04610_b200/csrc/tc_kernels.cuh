@@ -17,7 +17,7 @@ evo_status fwd(const evo_attn_desc* d, const Shape& s, const void* q, const void
                std::string* err);
 
 evo_status bwd(const evo_attn_desc* d, const Shape& s, const void* dout, const void* q,
-               const void* k, const void* v, const float* lse, const float* delta, void* dq,
+               const void* k, const void* v, const void* o, const float* lse, const float* delta, void* dq,
                void* dk, void* dv, float* dbias1, float* dbias2, void* scratch, cudaStream_t st,
                int* launches, std::string* err);
 

@@ -256,6 +256,16 @@ __device__ __forceinline__ uint64_t smem_desc(uint32_t saddr, uint32_t lbo, uint
   d |= (uint64_t)(layout & 7) << 61;
   return d;
 }
+// Split form for hot MMA loops: the high word (SBO, version, layout) is a compile-time constant and
+// the low word (start >> 4 | LBO >> 4 << 16) advances by plain integer adds.
+__host__ __device__ constexpr uint32_t desc_hi(uint32_t sbo, uint32_t layout) {
+  return ((sbo >> 4) & 0x3FFF) | (1u << 14) | ((layout & 7) << 29);
+}
+__device__ __forceinline__ uint32_t desc_lo(uint32_t saddr, uint32_t lbo) {
+  return ((saddr >> 4) & 0x3FFF) | (((lbo >> 4) & 0x3FFF) << 16);
+}
+__device__ __forceinline__ uint64_t desc_make(uint32_t lo, uint32_t hi) { return ((uint64_t)hi << 32) | lo; }
+
 // kind::f16 instruction descriptor: fp32 accumulate, A/B bf16 (fmt 1) or f16 (fmt 0)
 __host__ __device__ constexpr uint32_t instr_desc(int M, int N, bool f16, bool a_mn_major, bool b_mn_major) {
   return (1u << 4)                               // D format f32
