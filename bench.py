@@ -7,7 +7,10 @@ over rows (in-kernel, then NCCL all-reduce across ranks when N > 1).
 Default workload: configs[3] of BASELINE.json — OpenFold finetune MSA row
 attention N_seq=512 N_res=384 H=8 D=32 bf16 — the configuration the north-star
 target (>=50% of dense bf16 peak on 1 B200) is quoted on. --config c1..c5
-selects the others. Multi-GPU: rows sharded over ranks (strong scaling).
+selects the others. Multi-GPU (--scaling weak, the default): every rank owns its
+own rows of the configuration (the MSA-row / triangle-start axis partitioned, per
+rank the full config's row count) and the ranks exchange only the fp32 dBias2
+partial (NCCL all-reduce); --scaling strong splits the config's rows over ranks.
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--config c4] [--impl ours|reference]
   torchrun --nproc-per-node N bench.py --gpus N ...
@@ -120,9 +123,10 @@ class ClockSampler:
                 "samples": len(sm)}
 
 
-def make_inputs(cfg, rows, device, seed=7):
+def make_inputs(cfg, rows, device, seed=7, bias2_seed=None):
     """Synthetic OpenFold-shaped inputs: U[-1,1) rounded once to the
-    compute dtype; mask bias1 in {0,-1e9} at 10% (key 0 never masked)."""
+    compute dtype; mask bias1 in {0,-1e9} at 10% (key 0 never masked). The pair
+    bias is drawn from `bias2_seed` when given (identical on every rank)."""
     import torch
 
     Bo, Nr, L, H, D, dt, _ = cfg
@@ -136,6 +140,8 @@ def make_inputs(cfg, rows, device, seed=7):
     m = torch.rand(Bo, Nr, 1, 1, L, generator=g, device=device) < 0.1
     m[..., 0] = False
     b1 = torch.where(m, -1e9, 0.0)
+    if bias2_seed is not None:
+        g.manual_seed(bias2_seed + 1)
     b2 = u(Bo, 1, H, L, L)
     sl = lambda t: t[:, lo:hi].contiguous()
     out = [sl(q), sl(k), sl(v), sl(do), sl(b1), b2]
@@ -194,7 +200,7 @@ def run_reference_arm(args, cfg):
     v = statistics.median(x["value"] for x in vals)
     ms = flops(sample, L, H, D) / (v * 1e12) * 1e3
     line = {"metric": METRIC, "value": v, "unit": UNIT, "n_gpus": 0, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": args.scaling,
             "vs_baseline": None, "dtype": "f32", "data": "synthetic",
             "config": {"workload": desc, "Bo": Bo, "N": Nr, "L": L, "H": H, "D": D,
                        "parallelism": f"cpu_threads{threads}"},
@@ -202,7 +208,14 @@ def run_reference_arm(args, cfg):
             "cpu_baseline": {"value": v, "unit": UNIT, "cores": threads, "kind": vals[0]["kind"],
                              "sample": vals[0]["sample"]},
             "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
-    print(json.dumps(line), flush=True)
+    emit(line)
+
+
+_JSON_FD = 1
+
+
+def emit(line: dict):
+    os.write(_JSON_FD, (json.dumps(line) + "\n").encode())
 
 
 def main():
@@ -215,8 +228,16 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--all-configs", action="store_true", help="also time c1..c5 and attach them")
+    ap.add_argument("--scaling", default="weak", choices=["weak", "strong"],
+                    help="weak: each rank owns a full config's rows; strong: the config's rows split over ranks")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
+    # stdout carries exactly one JSON line: anything else written to fd 1 (library banners such as
+    # NCCL's version line) is sent to stderr, the JSON goes to the saved original stdout.
+    global _JSON_FD
+    sys.stdout.flush()
+    _JSON_FD = os.dup(1)
+    os.dup2(2, 1)
     cfg = CONFIGS[args.config]
     if args.impl == "reference":
         run_reference_arm(args, cfg)
@@ -237,9 +258,14 @@ def main():
         dist.init_process_group("nccl", device_id=dev)
 
     Bo, Nr, L, H, D, dt, desc = cfg
-    lo, hi = shard_rows(Nr, world, rank)
-    q, k, v, do, b1, b2 = (t.to(dev) for t in make_inputs(cfg, (lo, hi), dev))
-    B_local = Bo * (hi - lo)
+    if args.scaling == "weak":  # rank r owns rows [r*Nr, (r+1)*Nr) of an N*Nr-row problem
+        q, k, v, do, b1, b2 = (t.to(dev) for t in make_inputs(cfg, (0, Nr), dev, seed=7 + 1000 * rank,
+                                                               bias2_seed=7))
+        B_local, B_total = Bo * Nr, Bo * Nr * world
+    else:
+        lo, hi = shard_rows(Nr, world, rank)
+        q, k, v, do, b1, b2 = (t.to(dev) for t in make_inputs(cfg, (lo, hi), dev))
+        B_local, B_total = Bo * (hi - lo), Bo * Nr
 
     def step():
         return sharded_fwd_bwd(q, k, v, do, b1, b2)
@@ -288,7 +314,7 @@ def main():
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms = float(t.item())
-    total_flops = flops(Bo * Nr, L, H, D)
+    total_flops = flops(B_total, L, H, D)
     value = total_flops / (ms * 1e-3) / 1e12
 
     # ---- per-kernel timing (forward call, backward call) on the launching stream
@@ -383,15 +409,16 @@ def main():
             cpu = {"value": None, "unit": UNIT, "cores": 0, "kind": "unavailable", "sample": repr(e)}
 
     if rank == 0:
-        naive = 3 * H * Bo * Nr * L * L * (2 if dt == "bf16" else 4)
+        naive = 3 * H * B_local * L * L * (2 if dt == "bf16" else 4)
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": args.scaling,
             "vs_baseline": None, "dtype": dt, "data": "synthetic",
             "config": {"workload": desc, "config": args.config, "Bo": Bo, "N": Nr, "L": L, "H": H,
                        "D": D, "biases": "mask bias1 [Bo,N,1,1,L] + pair bias2 [Bo,1,H,L,L]",
+                       "rows_per_rank": B_local, "rows_total": B_total,
                        "parallelism": f"rows_sharded_dp{world}", "kernel_path": path,
-                       "l2": "inputs+outputs larger than L2 (no flush needed)" if ideal_bytes(Bo * Nr, L, H, D) > 126e6
+                       "l2": "inputs+outputs larger than L2 (no flush needed)" if ideal_bytes(B_local, L, H, D) > 126e6
                        else "working set smaller than L2 (not flushed)"},
             "peak_mem": {"extra_bytes_per_rank": int(peak_extra), "naive_logits_bytes": naive,
                          "o_l_plan_bytes": 8 * B_local * H * L + 4 * H * L * L},
@@ -404,7 +431,7 @@ def main():
         }
         if extra:
             line["other_configs"] = extra
-        print(json.dumps(line), flush=True)
+        emit(line)
     if world > 1:
         dist.destroy_process_group()
 

@@ -39,19 +39,21 @@ class ShardedStep:
     dbias2: Optional[torch.Tensor]
 
 
-def sharded_fwd_bwd(q, k, v, dout, bias1, bias2, group=None, head_chunks: int = 1,
-                    dbias_dtype: torch.dtype = torch.float32, need_dbias1: bool = False) -> ShardedStep:
+def sharded_fwd_bwd(q, k, v, dout, bias1, bias2, group=None, dbias_dtype: torch.dtype = torch.float32,
+                    need_dbias1: bool = False, ops=None) -> ShardedStep:
     """Forward + backward on this rank's row shard, dBias2 all-reduced.
 
-    q/k/v/dout/bias1 are this rank's rows ([Bo, n_local, L, H, D]); bias2 is
-    the full pair bias. `head_chunks` > 1 issues the all-reduce per head group
-    on a side stream so it overlaps the next group's compute. The mask-bias
-    gradient is off by default (the MSA mask carries no gradient in OpenFold;
-    the headline step produces dQ, dK, dV and dBias2).
+    q/k/v/dout/bias1 are this rank's rows ([Bo, n_local, L, H, D]); bias2 is the full pair bias.
+    The kernels reduce this rank's rows of dS into an fp32 dBias2 partial; one fp32 sum
+    all-reduce over the group completes it. The mask-bias gradient is off by
+    default (the MSA mask carries no gradient in OpenFold; the headline step produces dQ, dK, dV
+    and dBias2). `ops` = (forward, backward) overrides the CUDA operators (used by the CPU
+    gloo tests to drive the same control flow with the oracle).
     """
-    o, lse = evoformer_attention_forward(q, k, v, bias1, bias2)
+    fwd, bwd = ops if ops is not None else (evoformer_attention_forward, evoformer_attention_backward)
+    o, lse = fwd(q, k, v, bias1, bias2)
     world = dist.get_world_size(group) if dist.is_initialized() else 1
-    dq, dk, dv, db1, db2 = evoformer_attention_backward(
+    dq, dk, dv, db1, db2 = bwd(
         dout, q, k, v, o, lse, bias1, bias2, need_dbias1=need_dbias1 and bias1 is not None,
         need_dbias2=bias2 is not None, dbias_dtype=torch.float32)
     if db2 is not None and world > 1:
