@@ -19,8 +19,8 @@ LIB = os.path.join(LIBDIR, "libevoattn.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-I", os.path.join(ROOT, "include"),
-         "--expt-relaxed-constexpr", "-Xptxas", "-warn-spills"]
-SOURCES = ["evoattn_capi.cu", "tc_kernels.cu", "host_api.cu"]
+         "--expt-relaxed-constexpr", "-Xptxas", "-warn-spills"] + os.environ.get("EVO_NVCC_EXTRA", "").split()
+SOURCES = ["evoattn_capi.cu", "tc_kernels.cu"]
 
 
 def _sources():

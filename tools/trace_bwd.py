@@ -28,6 +28,8 @@ lib.evo_attn_debug_set_trace_bwd(None)
 t = buf.view(12, 64).cpu().tolist()
 t0 = min(x for row in t for x in row if x > 0)
 names = ["S_issue", "S_seen", "Pds_wg0", "Pds_wg1", "Grads", "Dq_seen", "Dq_out", "Q_full", "ProdQ", "K_full", "GradsSt", "S_done"]
+if "--phase" in sys.argv:  # library built with -DEVO_BWD_PHASE_TRACE=1
+    names[7:12] = ["ph_qfull", "ph_ldtm", "ph_math", "ph_sts", "ph_waits"]
 print("step " + " ".join(f"{n:>9s}" for n in names))
 for s in range(64):
     print(f"{s + 100:4d} " + " ".join(f"{(t[e][s] - t0) if t[e][s] else -1:9d}" for e in range(12)))
