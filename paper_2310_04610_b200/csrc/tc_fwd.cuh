@@ -36,7 +36,7 @@ constexpr float kRescaleThreshold = 8.f;  // log2 units
 template <int D>
 struct FwdCfg {
   static constexpr int NWG = D <= 32 ? 3 : 2;          // softmax warpgroups
-  static constexpr int kThreads = 64 + 128 * NWG;
+  static constexpr int kThreads = 32 + 160 * NWG;        // TMA warp + per warpgroup: UMMA warp, 4 softmax warps
   static constexpr int kRowBytes = D * 2;
   static constexpr int kTileQ = kBM * kRowBytes;       // Q tile
   static constexpr int kTileKV = kBN * kRowBytes;      // K or V tile
@@ -96,6 +96,8 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
 }
 
 // One CTA's item range, cut into segments at (ob, h, q-tile) boundaries. Inside a segment the
+constexpr int kPrefetchAhead = 2;  // K/V tiles pulled into L2 ahead of their shared-memory load
+
 // rows go out in groups of NWG (row s0 + g*NWG + w -> warpgroup w).
 struct Walker {
   long long t0, t1, N;
@@ -149,9 +151,11 @@ __global__ void __launch_bounds__(FwdCfg<D>::kThreads, 1)
   uint64_t* s_free = s_full + 2 * NWG;           // [NWG][2] PV reading that buffer done
   uint64_t* p_full = s_free + 2 * NWG;           // [NWG][2]
   uint64_t* o_free = p_full + 2 * NWG;           // [NWG] O read out at row end
-  uint64_t* kv_full = o_free + NWG;              // [stages]
-  uint64_t* kv_empty = kv_full + C::kStages;     // [stages]
-  uint64_t* bias_full = kv_empty + C::kStages;   // [nbias_slots]
+  uint64_t* kv_full = o_free + NWG;              // [stages] K tile landed
+  uint64_t* kv_empty = kv_full + C::kStages;     // [stages] S of that K tile done
+  uint64_t* v_full = kv_empty + C::kStages;      // [stages] V tile landed
+  uint64_t* v_empty = v_full + C::kStages;       // [stages] PV of that V tile done
+  uint64_t* bias_full = v_empty + C::kStages;    // [nbias_slots]
   uint64_t* bias_empty = bias_full + p.nbias_slots;
   uint32_t* tmem_slot = (uint32_t*)(bias_empty + p.nbias_slots);
 
@@ -168,11 +172,16 @@ __global__ void __launch_bounds__(FwdCfg<D>::kThreads, 1)
       ptx::mbar_init(&p_full[s], 128);
     }
     for (int w = 0; w < NWG; ++w) ptx::mbar_init(&o_free[w], 128);
-    for (int s = 0; s < C::kStages; ++s) { ptx::mbar_init(&kv_full[s], 1); ptx::mbar_init(&kv_empty[s], 1); }
+    for (int s = 0; s < C::kStages; ++s) {
+      ptx::mbar_init(&kv_full[s], 1);
+      ptx::mbar_init(&kv_empty[s], 1);
+      ptx::mbar_init(&v_full[s], 1);
+      ptx::mbar_init(&v_empty[s], 1);
+    }
     for (int s = 0; s < p.nbias_slots; ++s) { ptx::mbar_init(&bias_full[s], 1); ptx::mbar_init(&bias_empty[s], NWG); }
     ptx::fence_barrier_init();
   }
-  if (warp == 1) ptx::tmem_alloc(tmem_slot, 512);
+  if (warp == 0) ptx::tmem_alloc(tmem_slot, 512);
   ptx::tc_fence_before();
   __syncthreads();
   ptx::tc_fence_after();
@@ -184,13 +193,15 @@ __global__ void __launch_bounds__(FwdCfg<D>::kThreads, 1)
 
   if (warp == 0) {
     if (lane == 0) {
-      // ===================================================== TMA producer
+      // ===================================================== TMA producer (polling)
+      // Each warpgroup owns Q slots {2w, 2w+1} and K/V stages {2w, 2w+1}; K frees when its S
+      // completed, V when its PV completed. Within a group of rows the producer serves whichever
+      // warpgroup has a free slot, so a slow warpgroup never blocks the loads of the others.
       ptx::tma_prefetch(&tmQ); ptx::tma_prefetch(&tmK); ptx::tma_prefetch(&tmV);
       if (resident || streamed) ptx::tma_prefetch(&tmB2);
-      uint32_t qc[NWG];  // Q loads per warpgroup: slot = qc & 1, use parity = (qc >> 1) & 1
+      uint32_t qc[NWG], tk[NWG];  // per warpgroup: Q loads, K/V tiles of finished groups
 #pragma unroll
-      for (int w = 0; w < NWG; ++w) qc[w] = 0;
-      int ks = 0; uint32_t kph = 0;
+      for (int w = 0; w < NWG; ++w) qc[w] = tk[w] = 0;
       int bslot = 0; uint32_t bph = 0;
       const uint32_t b1_bytes = (uint32_t)p.L * 2;
       const bool b1t = p.bias1 && p.b1_tma;
@@ -198,6 +209,7 @@ __global__ void __launch_bounds__(FwdCfg<D>::kThreads, 1)
         const long long s1 = W.seg_end(s0);
         const SegInfo si = seg_info(s0, p);
         const int plane = si.ob * p.H + si.h;
+        const int row_end = si.ob * p.N + si.n0 + (int)(s1 - s0);
         if (resident) {
           for (int j = 0; j < p.nKT; ++j) {
             ptx::mbar_wait(&bias_empty[j], bph ^ 1);
@@ -209,136 +221,149 @@ __global__ void __launch_bounds__(FwdCfg<D>::kThreads, 1)
         int n = si.n0;
         for (long long a = s0; a < s1; a += NWG, n += NWG) {
           const int np = (int)min((long long)NWG, s1 - a);
+          uint32_t qdone = 0;
+          int jn[NWG], jv[NWG], jb = streamed ? 0 : p.nKT;
 #pragma unroll
-          for (int w = 0; w < NWG; ++w) {
-            if (w >= np) break;
-            const int b = si.ob * p.N + n + w;
-            const uint32_t slot = qc[w] & 1, ph = (qc[w] >> 1) & 1;
-            ptx::mbar_wait(&q_empty[w * 2 + slot], ph ^ 1);
-            ptx::mbar_expect_tx(&q_full[w * 2 + slot], C::kTileQ + (b1t ? b1_bytes : 0));
-            ptx::tma_load_4d(sQ + (w * 2 + slot) * C::kTileQ, &tmQ, &q_full[w * 2 + slot], 0, si.h, si.qt * kBM, b);
-            if (b1t)
-              bulk_g2s(sB1raw + (w * 2 + slot) * LP, (const uint16_t*)p.bias1 + (size_t)b * p.L, b1_bytes,
-                       &q_full[w * 2 + slot]);
-            ++qc[w];
-          }
-          for (int j = 0; j < p.nKT; ++j) {
-            if (streamed) {
-              ptx::mbar_wait(&bias_empty[bslot], bph ^ 1);
-              ptx::mbar_expect_tx(&bias_full[bslot], C::kBiasTile);
-              ptx::tma_load_3d(sBias + (size_t)bslot * C::kBiasTile, &tmB2, &bias_full[bslot], j * kBN,
-                               si.qt * kBM, plane);
-              if (++bslot == p.nbias_slots) { bslot = 0; bph ^= 1; }
-            }
+          for (int w = 0; w < NWG; ++w) jn[w] = jv[w] = w < np ? 0 : p.nKT;
+          for (;;) {
+            bool progress = false, done = jb >= p.nKT;
 #pragma unroll
             for (int w = 0; w < NWG; ++w) {
-              if (w >= np) break;
+              if (w >= np) continue;
               const int b = si.ob * p.N + n + w;
-              ptx::mbar_wait(&kv_empty[ks], kph ^ 1);
-              ptx::mbar_expect_tx(&kv_full[ks], 2 * C::kTileKV);
-              ptx::tma_load_4d(sK + ks * C::kTileKV, &tmK, &kv_full[ks], 0, si.h, j * kBN, b);
-              ptx::tma_load_4d(sV + ks * C::kTileKV, &tmV, &kv_full[ks], 0, si.h, j * kBN, b);
-              if (++ks == C::kStages) { ks = 0; kph ^= 1; }
+              if (!((qdone >> w) & 1)) {
+                const uint32_t slot = qc[w] & 1, ph = (qc[w] >> 1) & 1;
+                if (ptx::mbar_test(&q_empty[w * 2 + slot], ph ^ 1)) {
+                  ptx::mbar_expect_tx(&q_full[w * 2 + slot], C::kTileQ + (b1t ? b1_bytes : 0));
+                  ptx::tma_load_4d(sQ + (w * 2 + slot) * C::kTileQ, &tmQ, &q_full[w * 2 + slot], 0, si.h,
+                                   si.qt * kBM, b);
+                  if (b1t)
+                    bulk_g2s(sB1raw + (w * 2 + slot) * LP, (const uint16_t*)p.bias1 + (size_t)b * p.L, b1_bytes,
+                             &q_full[w * 2 + slot]);
+                  ++qc[w];
+                  qdone |= 1u << w;
+                  progress = true;
+                }
+              }
+              if (jn[w] < p.nKT) {
+                const uint32_t t = tk[w] + jn[w];
+                const int ks = w * 2 + (int)(t & 1);
+                if (ptx::mbar_test(&kv_empty[ks], ((t >> 1) & 1) ^ 1)) {
+                  ptx::mbar_expect_tx(&kv_full[ks], C::kTileKV);
+                  ptx::tma_load_4d(sK + ks * C::kTileKV, &tmK, &kv_full[ks], 0, si.h, jn[w] * kBN, b);
+                  // K/V tiles come from HBM with ~2 us latency under load: pull the ones
+                  // kPrefetchAhead further (or this warpgroup's next row's first ones) into L2
+                  const int ja = jn[w] + kPrefetchAhead;
+                  const int pb = ja < p.nKT ? b : b + NWG;
+                  if (pb < row_end) {
+                    const int pj = ja < p.nKT ? ja : ja - p.nKT;
+                    ptx::tma_prefetch_4d(&tmK, 0, si.h, pj * kBN, pb);
+                    ptx::tma_prefetch_4d(&tmV, 0, si.h, pj * kBN, pb);
+                  }
+                  ++jn[w];
+                  progress = true;
+                }
+              }
+              if (jv[w] < p.nKT) {
+                const uint32_t t = tk[w] + jv[w];
+                const int ks = w * 2 + (int)(t & 1);
+                if (ptx::mbar_test(&v_empty[ks], ((t >> 1) & 1) ^ 1)) {
+                  ptx::mbar_expect_tx(&v_full[ks], C::kTileKV);
+                  ptx::tma_load_4d(sV + ks * C::kTileKV, &tmV, &v_full[ks], 0, si.h, jv[w] * kBN, b);
+                  if (w == 0) trace(p, kTrKV, t);
+                  ++jv[w];
+                  progress = true;
+                }
+              }
+              done = done && ((qdone >> w) & 1) && jn[w] >= p.nKT && jv[w] >= p.nKT;
             }
+            if (jb < p.nKT && ptx::mbar_test(&bias_empty[bslot], bph ^ 1)) {  // streamed pair-bias ring
+              ptx::mbar_expect_tx(&bias_full[bslot], C::kBiasTile);
+              ptx::tma_load_3d(sBias + (size_t)bslot * C::kBiasTile, &tmB2, &bias_full[bslot], jb * kBN,
+                               si.qt * kBM, plane);
+              if (++bslot == p.nbias_slots) { bslot = 0; bph ^= 1; }
+              ++jb;
+              progress = true;
+            }
+            if (done) break;
+            if (!progress) __nanosleep(64);  // yield issue slots to the softmax warps
           }
+#pragma unroll
+          for (int w = 0; w < NWG; ++w)
+            if (w < np) tk[w] += p.nKT;
         }
       }
     }
-  } else if (warp == 1) {
+  } else if (warp <= NWG) {
+    // ===================================================== UMMA issuer of warpgroup w = warp - 1
+    // Waits only on this warpgroup's barriers: S(t) = Q K_t^T once K(t) landed and PV(t-2) released
+    // the S buffer; PV(t) = P(t) V_t (TS, P from TMEM) once the softmax wrote P(t) and V(t) landed.
+    const int w = warp - 1;
     if (lane == 0) {
-      // ===================================================== MMA issuer
       const uint32_t idS = ptx::instr_desc(kBM, kBN, F16, false, false);
       const uint32_t idO = ptx::instr_desc(kBM, D, F16, false, true);
-      uint32_t qc[NWG], tc[NWG], rc[NWG];  // per warpgroup: Q loads, tiles, rows
-#pragma unroll
-      for (int w = 0; w < NWG; ++w) qc[w] = tc[w] = rc[w] = 0;
-      int ks = 0; uint32_t kph = 0;
-      // PVs of the previous key tile, issued after the next tile's S MMAs
-      int pn = 0;
-      int pks[NWG];
-      uint32_t ptc[NWG];
-      bool pfirst[NWG];
-      auto issue_pvs = [&]() {
-#pragma unroll
-        for (int w = 0; w < NWG; ++w) {
-          if (w >= pn) break;
-          const uint32_t sb = ptc[w] & 1;
-          ptx::mbar_wait_spin(&p_full[w * 2 + sb], (ptc[w] >> 1) & 1);
-          if (pfirst[w]) {  // first tile of a row overwrites O: the previous row must be read out
-            ptx::mbar_wait_spin(&o_free[w], (rc[w] & 1) ^ 1);
-            ++rc[w];
-          }
-          ptx::tc_fence_after();
-          const uint32_t vbase = ptx::smem_u32(sV + pks[w] * C::kTileKV);
-          const uint32_t wbase = tmem + w * C::kWGcols;
-#pragma unroll
-          for (int kk = 0; kk < kBN / 16; ++kk) {
-            // V is MN-major: 16 keys = two 8-row swizzle atoms (SBO = 8 rows)
-            const uint64_t bd = ptx::smem_desc(vbase + kk * 16 * C::kRowBytes, 16 * C::kRowBytes,
-                                               8 * C::kRowBytes, kSw);
-            ptx::mma_ts(wbase + 128, wbase + sb * 64 + kk * 8, bd, idO, (!pfirst[w] || kk > 0) ? 1u : 0u);
-          }
-          ptx::tc_commit(&s_free[w * 2 + sb]);
-          ptx::tc_commit(&kv_empty[pks[w]]);
-          trace(p, kTrPV, ptc[w] * 4 + w);
+      const uint32_t wbase = tmem + w * C::kWGcols;
+      uint32_t qc = 0, t = 0, rc = 0;
+      auto do_pv = [&](uint32_t T, bool first) {
+        const uint32_t sb = T & 1;
+        const int ks = w * 2 + (int)(T & 1);
+        ptx::mbar_wait_spin(&p_full[w * 2 + sb], (T >> 1) & 1);
+        if (w == 0) trace(p, 8, T);
+        ptx::mbar_wait_spin(&v_full[ks], (T >> 1) & 1);
+        if (w == 0) trace(p, 9, T);
+        if (first) {  // first tile of a row overwrites O: the previous row must be read out
+          ptx::mbar_wait_spin(&o_free[w], (rc & 1) ^ 1);
+          ++rc;
         }
-        pn = 0;
+        ptx::tc_fence_after();
+        const uint32_t vbase = ptx::smem_u32(sV + ks * C::kTileKV);
+#pragma unroll
+        for (int kk = 0; kk < kBN / 16; ++kk) {
+          // V is MN-major: 16 keys = two 8-row swizzle atoms (SBO = 8 rows)
+          const uint64_t bd =
+              ptx::smem_desc(vbase + kk * 16 * C::kRowBytes, 16 * C::kRowBytes, 8 * C::kRowBytes, kSw);
+          ptx::mma_ts(wbase + 128, wbase + sb * 64 + kk * 8, bd, idO, (!first || kk > 0) ? 1u : 0u);
+        }
+        ptx::tc_commit(&s_free[w * 2 + sb]);
+        ptx::tc_commit(&v_empty[ks]);
+        if (w == 0) trace(p, kTrPV, T);
       };
       for (long long s0 = W.t0; s0 < W.t1; s0 = W.seg_end(s0)) {
         const long long s1 = W.seg_end(s0);
-        for (long long a = s0; a < s1; a += NWG) {
-          const int np = (int)min((long long)NWG, s1 - a);
-          for (int j = 0; j < p.nKT; ++j) {
-            int cks[NWG];
-            uint32_t ctc[NWG];
+        for (long long a = s0 + w; a < s1; a += NWG) {
+          const uint32_t qs = qc & 1;
+          for (int j = 0; j < p.nKT; ++j, ++t) {
+            const uint32_t sb = t & 1;
+            const int ks = w * 2 + (int)(t & 1);
+            if (j == 0) ptx::mbar_wait_spin(&q_full[w * 2 + qs], (qc >> 1) & 1);
+            ptx::mbar_wait_spin(&kv_full[ks], (t >> 1) & 1);
+            ptx::mbar_wait_spin(&s_free[w * 2 + sb], ((t >> 1) & 1) ^ 1);
+            ptx::tc_fence_after();
+            const uint32_t qbase = ptx::smem_u32(sQ + (w * 2 + qs) * C::kTileQ);
+            const uint32_t kbase = ptx::smem_u32(sK + ks * C::kTileKV);
 #pragma unroll
-            for (int w = 0; w < NWG; ++w) {
-              if (w >= np) break;
-              const uint32_t qs = qc[w] & 1;
-              if (j == 0) ptx::mbar_wait_spin(&q_full[w * 2 + qs], (qc[w] >> 1) & 1);
-              const uint32_t sb = tc[w] & 1;
-              ptx::mbar_wait_spin(&kv_full[ks], kph);
-              ptx::mbar_wait_spin(&s_free[w * 2 + sb], ((tc[w] >> 1) & 1) ^ 1);
-              ptx::tc_fence_after();
-              const uint32_t qbase = ptx::smem_u32(sQ + (w * 2 + qs) * C::kTileQ);
-              const uint32_t kbase = ptx::smem_u32(sK + ks * C::kTileKV);
-#pragma unroll
-              for (int kk = 0; kk < D / 16; ++kk) {
-                const uint64_t ad = ptx::smem_desc(qbase + kk * 32, 16, 8 * C::kRowBytes, kSw);
-                const uint64_t bd = ptx::smem_desc(kbase + kk * 32, 16, 8 * C::kRowBytes, kSw);
-                ptx::mma_ss(tmem + w * C::kWGcols + sb * 64, ad, bd, idS, kk > 0);
-              }
-              ptx::tc_commit(&s_full[w * 2 + sb]);
-              trace(p, kTrS, tc[w] * 4 + w);
-              if (j == p.nKT - 1) {
-                ptx::tc_commit(&q_empty[w * 2 + qs]);
-                ++qc[w];
-              }
-              cks[w] = ks;
-              ctc[w] = tc[w];
-              ++tc[w];
-              if (++ks == C::kStages) { ks = 0; kph ^= 1; }
+            for (int kk = 0; kk < D / 16; ++kk) {
+              const uint64_t ad = ptx::smem_desc(qbase + kk * 32, 16, 8 * C::kRowBytes, kSw);
+              const uint64_t bd = ptx::smem_desc(kbase + kk * 32, 16, 8 * C::kRowBytes, kSw);
+              ptx::mma_ss(wbase + sb * 64, ad, bd, idS, kk > 0);
             }
-            issue_pvs();
-            pn = np;
-#pragma unroll
-            for (int w = 0; w < NWG; ++w) {
-              if (w >= np) break;
-              pks[w] = cks[w];
-              ptc[w] = ctc[w];
-              pfirst[w] = (j == 0);
-            }
+            ptx::tc_commit(&s_full[w * 2 + sb]);
+            ptx::tc_commit(&kv_empty[ks]);  // the K stage may be refilled once S completed
+            if (w == 0) trace(p, kTrS, t);
+            if (j == p.nKT - 1) ptx::tc_commit(&q_empty[w * 2 + qs]);
+            if (j > 0) do_pv(t - 1, j == 1);
           }
+          do_pv(t - 1, p.nKT == 1);
+          ++qc;
         }
       }
-      issue_pvs();
     }
   } else {
     // ===================================================== softmax warpgroups
-    const int wg = (warp - 2) / 4;
+    const int wg = (warp - 1 - NWG) / 4;
     const int q4 = warp & 3;                  // TMEM lane quadrant
     const int r = q4 * 32 + lane;             // query row in tile == TMEM lane
-    const int tid_wg = (warp - 2 - 4 * wg) * 32 + lane;
+    const int tid_wg = (warp - 1 - NWG - 4 * wg) * 32 + lane;
     const uint32_t lane_off = (uint32_t)(q4 * 32) << 16;
     const uint32_t tbase = tmem + lane_off + wg * C::kWGcols;
     const uint32_t o_tmem = tbase + 128;
@@ -550,7 +575,7 @@ __global__ void __launch_bounds__(FwdCfg<D>::kThreads, 1)
   }
   ptx::tc_fence_before();
   __syncthreads();
-  if (warp == 1) {
+  if (warp == 0) {
     ptx::tc_fence_after();
     ptx::tmem_dealloc(tmem, 512);
   }

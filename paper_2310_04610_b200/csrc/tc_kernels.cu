@@ -88,7 +88,7 @@ size_t fwd_smem_bytes(int nbias_slots, int nKT) {
   b += (size_t)C::NWG * 2 * C::kTileQ + 2 * (size_t)C::kStages * C::kTileKV;
   b += (size_t)nbias_slots * C::kBiasTile;
   b += (size_t)C::NWG * 2 * LP * (2 + 4);  // bias1 row: raw bf16 + fp32, double buffered per WG
-  b += (size_t)(11 * C::NWG + 2 * C::kStages + 2 * nbias_slots) * 8 + 16;
+  b += (size_t)(11 * C::NWG + 4 * C::kStages + 2 * nbias_slots) * 8 + 16;
   return b;
 }
 
