@@ -57,6 +57,8 @@ struct FwdParams {
   int bias_mode;
   int nbias_slots;   // resident: nKT; streamed: 3
   int b1_tma;        // bias1 rows fetched by TMA bulk copy (L % 8 == 0)
+  int aug;           // bias1 / key mask enter S as one extra K=16 MMA step (bias1 present or L % 64 != 0)
+  uint32_t aug_c;    // (c_lo << 16) | c_hi: 16-bit two-term split of 1/scale
   const void* bias1;  // [B, L] or null
   const void* bias2;  // [Bo, H, L, L] (read directly in kBiasGlobal mode)
   void* o;           // [B, L, H, D]
@@ -96,7 +98,8 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
 }
 
 // One CTA's item range, cut into segments at (ob, h, q-tile) boundaries. Inside a segment the
-constexpr int kPrefetchAhead = 2;  // K/V tiles pulled into L2 ahead of their shared-memory load
+constexpr int kPrefetchAhead = 2;
+constexpr int kAugA = kBM * 32, kAugB = kBN * 32;  // bias1 augmentation tiles (16 bf16 per row)  // K/V tiles pulled into L2 ahead of their shared-memory load
 
 // rows go out in groups of NWG (row s0 + g*NWG + w -> warpgroup w).
 struct Walker {
@@ -142,11 +145,12 @@ __global__ void __launch_bounds__(FwdCfg<D>::kThreads, 1)
   uint8_t* sK = sQ + NWG * 2 * C::kTileQ;                   // [stages]
   uint8_t* sV = sK + C::kStages * C::kTileKV;               // [stages]
   uint8_t* sBias = sV + C::kStages * C::kTileKV;            // [nbias_slots] x 16 KB
-  uint16_t* sB1raw = (uint16_t*)(sBias + (size_t)p.nbias_slots * C::kBiasTile);  // [NWG][2][LP] bf16
-  float* sB1 = (float*)(sB1raw + NWG * 2 * LP);              // [NWG][2][LP] fp32 * log2e
-  uint64_t* bars = (uint64_t*)(sB1 + NWG * 2 * LP);
+  uint8_t* sAaug = sBias + (size_t)p.nbias_slots * C::kBiasTile;  // 128 x 16: (c_hi, c_lo, 0..), SW32
+  uint8_t* sBaug = sAaug + kAugA;                            // [stages] 64 x 16: (bias1, bias1, 0..), SW32
+  uint16_t* sB1raw = (uint16_t*)(sBaug + C::kStages * kAugB);  // [NWG][2][LP] bias1 rows (raw)
+  uint64_t* bars = (uint64_t*)(sB1raw + NWG * 2 * LP);
   uint64_t* q_full = bars;                       // [NWG][2] Q (+ bias1 row) landed
-  uint64_t* q_empty = q_full + 2 * NWG;          // [NWG][2] MMA commit + the warpgroup
+  uint64_t* q_empty = q_full + 2 * NWG;          // [NWG][2] last S of the row done
   uint64_t* s_full = q_empty + 2 * NWG;          // [NWG][2]
   uint64_t* s_free = s_full + 2 * NWG;           // [NWG][2] PV reading that buffer done
   uint64_t* p_full = s_free + 2 * NWG;           // [NWG][2]
@@ -166,7 +170,7 @@ __global__ void __launch_bounds__(FwdCfg<D>::kThreads, 1)
   if (threadIdx.x == 0) {
     for (int s = 0; s < 2 * NWG; ++s) {
       ptx::mbar_init(&q_full[s], 1);
-      ptx::mbar_init(&q_empty[s], 2);
+      ptx::mbar_init(&q_empty[s], 1);
       ptx::mbar_init(&s_full[s], 1);
       ptx::mbar_init(&s_free[s], 1);
       ptx::mbar_init(&p_full[s], 128);
@@ -181,6 +185,16 @@ __global__ void __launch_bounds__(FwdCfg<D>::kThreads, 1)
     for (int s = 0; s < p.nbias_slots; ++s) { ptx::mbar_init(&bias_full[s], 1); ptx::mbar_init(&bias_empty[s], NWG); }
     ptx::fence_barrier_init();
   }
+  // A_aug: row i = (c_hi, c_lo, 0, ...); with B_aug row j = (bias1[j], bias1[j], 0, ...) one extra K=16
+  // step of S = Q K^T adds bias1[j] / scale exactly to ~2^-16 (16B chunk 0 of a 32B row sits at chunk
+  // (row >> 2) & 1 under the 32B swizzle).
+  for (int i = threadIdx.x; i < kBM; i += blockDim.x) {
+    const uint32_t c = (uint32_t)((i >> 2) & 1);
+    uint4* row = (uint4*)(sAaug + i * 32);
+    row[c] = make_uint4(p.aug_c, 0u, 0u, 0u);
+    row[c ^ 1] = make_uint4(0u, 0u, 0u, 0u);
+  }
+  ptx::fence_proxy_async_smem();
   if (warp == 0) ptx::tmem_alloc(tmem_slot, 512);
   ptx::tc_fence_before();
   __syncthreads();
@@ -299,58 +313,93 @@ __global__ void __launch_bounds__(FwdCfg<D>::kThreads, 1)
     // Waits only on this warpgroup's barriers: S(t) = Q K_t^T once K(t) landed and PV(t-2) released
     // the S buffer; PV(t) = P(t) V_t (TS, P from TMEM) once the softmax wrote P(t) and V(t) landed.
     const int w = warp - 1;
-    if (lane == 0) {
+    {
       const uint32_t idS = ptx::instr_desc(kBM, kBN, F16, false, false);
       const uint32_t idO = ptx::instr_desc(kBM, D, F16, false, true);
+      constexpr uint32_t kHiAug = ptx::desc_hi(256, 6);  // 32-byte rows, SW32
+      const uint64_t aAug = ptx::desc_make(ptx::desc_lo(ptx::smem_u32(sAaug), 16), kHiAug);
       const uint32_t wbase = tmem + w * C::kWGcols;
       uint32_t qc = 0, t = 0, rc = 0;
       auto do_pv = [&](uint32_t T, bool first) {
         const uint32_t sb = T & 1;
         const int ks = w * 2 + (int)(T & 1);
         ptx::mbar_wait_spin(&p_full[w * 2 + sb], (T >> 1) & 1);
-        if (w == 0) trace(p, 8, T);
+        if (w == 0 && lane == 0) trace(p, 8, T);
         ptx::mbar_wait_spin(&v_full[ks], (T >> 1) & 1);
-        if (w == 0) trace(p, 9, T);
+        if (w == 0 && lane == 0) trace(p, 9, T);
         if (first) {  // first tile of a row overwrites O: the previous row must be read out
           ptx::mbar_wait_spin(&o_free[w], (rc & 1) ^ 1);
           ++rc;
         }
         ptx::tc_fence_after();
-        const uint32_t vbase = ptx::smem_u32(sV + ks * C::kTileKV);
+        if (ptx::elect_one()) {
+          const uint32_t vbase = ptx::smem_u32(sV + ks * C::kTileKV);
 #pragma unroll
-        for (int kk = 0; kk < kBN / 16; ++kk) {
-          // V is MN-major: 16 keys = two 8-row swizzle atoms (SBO = 8 rows)
-          const uint64_t bd =
-              ptx::smem_desc(vbase + kk * 16 * C::kRowBytes, 16 * C::kRowBytes, 8 * C::kRowBytes, kSw);
-          ptx::mma_ts(wbase + 128, wbase + sb * 64 + kk * 8, bd, idO, (!first || kk > 0) ? 1u : 0u);
+          for (int kk = 0; kk < kBN / 16; ++kk) {
+            // V is MN-major: 16 keys = two 8-row swizzle atoms (SBO = 8 rows)
+            const uint64_t bd =
+                ptx::smem_desc(vbase + kk * 16 * C::kRowBytes, 16 * C::kRowBytes, 8 * C::kRowBytes, kSw);
+            ptx::mma_ts(wbase + 128, wbase + sb * 64 + kk * 8, bd, idO, (!first || kk > 0) ? 1u : 0u);
+          }
+          ptx::tc_commit(&s_free[w * 2 + sb]);
+          ptx::tc_commit(&v_empty[ks]);
+          if (w == 0) trace(p, kTrPV, T);
         }
-        ptx::tc_commit(&s_free[w * 2 + sb]);
-        ptx::tc_commit(&v_empty[ks]);
-        if (w == 0) trace(p, kTrPV, T);
+        __syncwarp();
       };
       for (long long s0 = W.t0; s0 < W.t1; s0 = W.seg_end(s0)) {
         const long long s1 = W.seg_end(s0);
+        const SegInfo si = seg_info(s0, p);
         for (long long a = s0 + w; a < s1; a += NWG) {
           const uint32_t qs = qc & 1;
+          const int b = si.ob * p.N + si.n0 + (int)(a - s0);
           for (int j = 0; j < p.nKT; ++j, ++t) {
             const uint32_t sb = t & 1;
             const int ks = w * 2 + (int)(t & 1);
             if (j == 0) ptx::mbar_wait_spin(&q_full[w * 2 + qs], (qc >> 1) & 1);
-            ptx::mbar_wait_spin(&kv_full[ks], (t >> 1) & 1);
+            ptx::mbar_wait_spin(&kv_full[ks], (t >> 1) & 1);  // K(t) landed; B_aug slot ks is free
+            if (p.aug) {
+              // B_aug row jj = (bias1[j0 + jj], same or 0 if non-finite) for keys < L, (-inf, 0) past L
+#pragma unroll
+              for (int h2 = 0; h2 < 2; ++h2) {
+                const int jj = lane + 32 * h2, key = j * kBN + jj;
+                uint32_t v0 = 0u, v1 = 0u;
+                if (key >= p.L) {
+                  v0 = F16 ? 0xFC00u : 0xFF80u;
+                } else if (p.bias1) {
+                  v0 = p.b1_tma ? (uint32_t)sB1raw[(w * 2 + qs) * LP + key]
+                                : (uint32_t)((const uint16_t*)p.bias1)[(size_t)b * p.L + key];
+                  const bool fin = F16 ? (v0 & 0x7C00u) != 0x7C00u : (v0 & 0x7F80u) != 0x7F80u;
+                  v1 = fin ? v0 : 0u;
+                }
+                const uint32_t c = (uint32_t)((jj >> 2) & 1);
+                uint4* row = (uint4*)(sBaug + ks * kAugB + jj * 32);
+                row[c] = make_uint4(v0 | (v1 << 16), 0u, 0u, 0u);
+                row[c ^ 1] = make_uint4(0u, 0u, 0u, 0u);
+              }
+              ptx::fence_proxy_async_smem();
+              __syncwarp();
+            }
             ptx::mbar_wait_spin(&s_free[w * 2 + sb], ((t >> 1) & 1) ^ 1);
             ptx::tc_fence_after();
-            const uint32_t qbase = ptx::smem_u32(sQ + (w * 2 + qs) * C::kTileQ);
-            const uint32_t kbase = ptx::smem_u32(sK + ks * C::kTileKV);
+            if (ptx::elect_one()) {
+              const uint32_t qbase = ptx::smem_u32(sQ + (w * 2 + qs) * C::kTileQ);
+              const uint32_t kbase = ptx::smem_u32(sK + ks * C::kTileKV);
 #pragma unroll
-            for (int kk = 0; kk < D / 16; ++kk) {
-              const uint64_t ad = ptx::smem_desc(qbase + kk * 32, 16, 8 * C::kRowBytes, kSw);
-              const uint64_t bd = ptx::smem_desc(kbase + kk * 32, 16, 8 * C::kRowBytes, kSw);
-              ptx::mma_ss(wbase + sb * 64, ad, bd, idS, kk > 0);
+              for (int kk = 0; kk < D / 16; ++kk) {
+                const uint64_t ad = ptx::smem_desc(qbase + kk * 32, 16, 8 * C::kRowBytes, kSw);
+                const uint64_t bd = ptx::smem_desc(kbase + kk * 32, 16, 8 * C::kRowBytes, kSw);
+                ptx::mma_ss(wbase + sb * 64, ad, bd, idS, kk > 0);
+              }
+              if (p.aug)
+                ptx::mma_ss(wbase + sb * 64, aAug,
+                            ptx::desc_make(ptx::desc_lo(ptx::smem_u32(sBaug + ks * kAugB), 16), kHiAug), idS, 1u);
+              ptx::tc_commit(&s_full[w * 2 + sb]);
+              ptx::tc_commit(&kv_empty[ks]);  // the K stage (and its B_aug rows) may be refilled once S completed
+              if (w == 0) trace(p, kTrS, t);
+              if (j == p.nKT - 1) ptx::tc_commit(&q_empty[w * 2 + qs]);
             }
-            ptx::tc_commit(&s_full[w * 2 + sb]);
-            ptx::tc_commit(&kv_empty[ks]);  // the K stage may be refilled once S completed
-            if (w == 0) trace(p, kTrS, t);
-            if (j == p.nKT - 1) ptx::tc_commit(&q_empty[w * 2 + qs]);
+            __syncwarp();
             if (j > 0) do_pv(t - 1, j == 1);
           }
           do_pv(t - 1, p.nKT == 1);
@@ -371,7 +420,7 @@ __global__ void __launch_bounds__(FwdCfg<D>::kThreads, 1)
     const uint32_t r7 = (uint32_t)(r & 7) << 4;  // 128B swizzle: chunk c of row r -> (c ^ (r & 7))
     const float2 scl2 = make_float2(p.scale_log2, p.scale_log2);
     const float2 lg2 = make_float2(kLog2e, kLog2e);
-    uint32_t qc = 0, tcount = 0;
+    uint32_t tcount = 0;
     int bslot = 0; uint32_t bph = 0;
 
     for (long long s0 = W.t0; s0 < W.t1; s0 = W.seg_end(s0)) {
@@ -399,30 +448,8 @@ __global__ void __launch_bounds__(FwdCfg<D>::kThreads, 1)
         }
         const int b = si.ob * p.N + n + wg;
         const bool last_row = a + NWG >= s1;
-        // ---- bias1 row -> fp32 * log2e in this warpgroup's slot; keys >= L -> -inf
-        const uint32_t qs = qc & 1;
-        float* b1s = sB1 + (wg * 2 + qs) * LP;
-        ptx::mbar_wait(&q_full[wg * 2 + qs], (qc >> 1) & 1);
+        // bias1 and the key mask past L are already inside S (the UMMA warp's augmentation step)
         if (tid_wg == 0 && wg == 0) trace(p, kTrRowStart, tcount);
-        ptx::named_bar_sync(1 + wg, 128);  // previous readers of this slot are done
-        const uint16_t* rawrow = sB1raw + (wg * 2 + qs) * LP;
-        for (int j = tid_wg; j < LP; j += 128) {
-          float v = -INFINITY;
-          if (j < p.L) {
-            if (!p.bias1) v = 0.f;
-            else if (p.b1_tma) {
-              const unsigned short u = rawrow[j];
-              v = (F16 ? __half2float(__ushort_as_half(u)) : __uint_as_float((uint32_t)u << 16)) * kLog2e;
-            } else {
-              v = load_half<F16>(p.bias1, (size_t)b * p.L + j) * kLog2e;
-            }
-          }
-          b1s[j] = v;
-        }
-        ptx::named_bar_sync(1 + wg, 128);
-        if (tid_wg == 0) ptx::mbar_arrive(&q_empty[wg * 2 + qs]);  // raw bias1 row consumed
-        ++qc;
-        const uint32_t b1s_addr = ptx::smem_u32(b1s);
 
         float m_run = -INFINITY, l_run = 0.f;
         for (int j = 0; j < p.nKT; ++j) {
@@ -440,7 +467,7 @@ __global__ void __launch_bounds__(FwdCfg<D>::kThreads, 1)
           if (streamed) { slot = bslot; ptx::mbar_wait(&bias_full[slot], bph); }
           ptx::tmem_ld_wait();
           auto sv = [&](int k) { return __uint_as_float(k < 32 ? ra[k & 31] : rb[k & 31]); };
-          // ---- x = S*scale*log2e + bias2*log2e + bias1*log2e   (log2 domain)
+          // ---- x = (S + bias1/scale) * scale * log2e + bias2 * log2e   (log2 domain)
           float2 x[32];
           if constexpr (resident || streamed) {
             // 128B-swizzled bias tile: 8-key chunk c of row r sits at chunk c ^ (r & 7)
@@ -448,34 +475,22 @@ __global__ void __launch_bounds__(FwdCfg<D>::kThreads, 1)
 #pragma unroll
             for (int c = 0; c < 8; ++c) {
               const uint4 raw = lds128(bt + ((uint32_t)(c << 4) ^ r7));
-              const uint4 w0 = lds128(b1s_addr + (j0 + c * 8) * 4);
-              const uint4 w1 = lds128(b1s_addr + (j0 + c * 8 + 4) * 4);
               const uint32_t wv[4] = {raw.x, raw.y, raw.z, raw.w};
-              const uint32_t bw[8] = {w0.x, w0.y, w0.z, w0.w, w1.x, w1.y, w1.z, w1.w};
 #pragma unroll
-              for (int e = 0; e < 4; ++e) {
-                const float2 bb = __ffma2_rn(unpack2<F16>(wv[e]), lg2,
-                                             make_float2(__uint_as_float(bw[2 * e]), __uint_as_float(bw[2 * e + 1])));
-                x[c * 4 + e] = __ffma2_rn(make_float2(sv(c * 8 + 2 * e), sv(c * 8 + 2 * e + 1)), scl2, bb);
-              }
+              for (int e = 0; e < 4; ++e)
+                x[c * 4 + e] = __ffma2_rn(unpack2<F16>(wv[e]), lg2,
+                                          __fmul2_rn(make_float2(sv(c * 8 + 2 * e), sv(c * 8 + 2 * e + 1)), scl2));
             }
           } else if constexpr (BM == kBiasGlobal) {
 #pragma unroll
             for (int k = 0; k < kBN; k += 2) {
               const int ja = min(j0 + k, p.L - 1), jb = min(j0 + k + 1, p.L - 1);
               const float2 bv = make_float2(load_half<F16>(b2row, ja), load_half<F16>(b2row, jb));
-              const float2 b1v = make_float2(b1s[j0 + k], b1s[j0 + k + 1]);
-              x[k / 2] = __ffma2_rn(make_float2(sv(k), sv(k + 1)), scl2, __ffma2_rn(bv, lg2, b1v));
+              x[k / 2] = __ffma2_rn(make_float2(sv(k), sv(k + 1)), scl2, __fmul2_rn(bv, lg2));
             }
           } else {
 #pragma unroll
-            for (int k = 0; k < kBN; k += 4) {
-              const uint4 wu = lds128(b1s_addr + (j0 + k) * 4);
-              x[k / 2] = __ffma2_rn(make_float2(sv(k), sv(k + 1)), scl2,
-                                    make_float2(__uint_as_float(wu.x), __uint_as_float(wu.y)));
-              x[k / 2 + 1] = __ffma2_rn(make_float2(sv(k + 2), sv(k + 3)), scl2,
-                                        make_float2(__uint_as_float(wu.z), __uint_as_float(wu.w)));
-            }
+            for (int k = 0; k < kBN; k += 2) x[k / 2] = __fmul2_rn(make_float2(sv(k), sv(k + 1)), scl2);
           }
           // ---- bias release: streamed tiles per use; the resident block after the segment's last use
           if (streamed || (resident && last_row && j == p.nKT - 1)) {

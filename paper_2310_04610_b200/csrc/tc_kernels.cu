@@ -87,12 +87,31 @@ size_t fwd_smem_bytes(int nbias_slots, int nKT) {
   size_t b = 1024;  // alignment slack
   b += (size_t)C::NWG * 2 * C::kTileQ + 2 * (size_t)C::kStages * C::kTileKV;
   b += (size_t)nbias_slots * C::kBiasTile;
-  b += (size_t)C::NWG * 2 * LP * (2 + 4);  // bias1 row: raw bf16 + fp32, double buffered per WG
+  b += (size_t)kAugA + (size_t)C::kStages * kAugB;  // bias1 augmentation tiles
+  b += (size_t)C::NWG * 2 * LP * 2;                 // bias1 rows (raw), double buffered per WG
   b += (size_t)(11 * C::NWG + 4 * C::kStages + 2 * nbias_slots) * 8 + 16;
   return b;
 }
 
 constexpr size_t kMaxSmem = 227 * 1024;
+
+// 16-bit two-term split of c (c ~= hi + lo) packed as (lo << 16) | hi, for the bias1 augmentation
+// step: an exact-to-~2^-16 multiplier carried by a bf16/f16 UMMA operand.
+uint32_t aug_split(double c, bool f16) {
+  uint16_t hi, lo;
+  if (f16) {
+    const __half h = __double2half(c);
+    const __half l = __double2half(c - (double)__half2float(h));
+    hi = *(const uint16_t*)&h;
+    lo = *(const uint16_t*)&l;
+  } else {
+    const __nv_bfloat16 h = __double2bfloat16(c);
+    const __nv_bfloat16 l = __double2bfloat16(c - (double)__bfloat162float(h));
+    hi = *(const uint16_t*)&h;
+    lo = *(const uint16_t*)&l;
+  }
+  return (uint32_t)hi | ((uint32_t)lo << 16);
+}
 
 template <int D, bool F16>
 evo_status launch_fwd(const evo_attn_desc* d, const Shape& s, const void* q, const void* k, const void* v,
@@ -117,6 +136,8 @@ evo_status launch_fwd(const evo_attn_desc* d, const Shape& s, const void* q, con
   p.bias_mode = kBiasNone;
   p.nbias_slots = 0;
   p.b1_tma = (s.L % 8 == 0) ? 1 : 0;
+  p.aug = (s.bias1 != nullptr || s.L % kBN != 0) ? 1 : 0;
+  p.aug_c = aug_split(1.0 / (double)s.scale, F16);
   if (s.bias2) {
     if (s.L % 8 != 0) {
       p.bias_mode = kBiasGlobal;
@@ -222,22 +243,7 @@ evo_status launch_bwd(const evo_attn_desc* d, const Shape& s, const void* dout, 
   // bias1 (and the key mask past L) enter S through one extra K=16 MMA step: A_aug rows hold a
   // 16-bit two-term split of 1/scale, B_aug rows the bias1 value of each key.
   p.aug = (s.bias1 != nullptr || s.L % bk::kBN != 0) ? 1 : 0;
-  {
-    const double c = 1.0 / (double)s.scale;
-    uint16_t hi, lo;
-    if (F16) {
-      const __half h = __double2half(c);
-      const __half l = __double2half(c - (double)__half2float(h));
-      hi = *(const uint16_t*)&h;
-      lo = *(const uint16_t*)&l;
-    } else {
-      const __nv_bfloat16 h = __double2bfloat16(c);
-      const __nv_bfloat16 l = __double2bfloat16(c - (double)__bfloat162float(h));
-      hi = *(const uint16_t*)&h;
-      lo = *(const uint16_t*)&l;
-    }
-    p.aug_c = (uint32_t)hi | ((uint32_t)lo << 16);
-  }
+  p.aug_c = aug_split(1.0 / (double)s.scale, F16);
   const size_t smem = bwd_smem_bytes<D>(p.nQT);
   if (smem > kMaxSmem) {
     *err = "backward shared-memory budget exceeded";
