@@ -57,14 +57,16 @@ struct Cfg {
 struct Params {
   int B, N, L, H, Bo;
   int nQT, nKT;
-  long long total;   // items = Bo*H*nKT*N
+  int nQC, nIC;      // query tiles per chunk (<= 3: the dBias2 strip of a chunk fits TMEM), chunks
+  long long total;   // items = Bo*H*nKT*nIC*N
   int aligned, split;
   float scale, scale_log2;
   const void* bias1;    // [B, L] or null
   const float* lse2;    // [B, H, nQT*128] lse * log2e, +inf past L
   const float* delta;   // [B, H, nQT*128] rowsum(dO * O), 0 past L
-  void* dk;             // [B, L, H, D]
+  void* dk;             // [B, L, H, D] (nIC == 1: written directly)
   void* dv;
+  int dkv_reduce;       // nIC > 1: dK/dV partials of each query chunk reduce-add into fp32 accumulators
   float* dbias2;        // [Bo, H, L, L] fp32 accumulator or null
   int has_bias2;
   int aug;             // extra K-step adding bias1 / scale (bias1 present or L % 64 != 0)
@@ -96,16 +98,20 @@ __device__ __forceinline__ Walker make_walker(const Params& p) {
   return Walker{p.total * blockIdx.x / gridDim.x, p.total * (blockIdx.x + 1) / gridDim.x, p.N};
 }
 struct Unit {
-  int ob, h, jt, n0;
+  int ob, h, jt, ic, it0, it1, n0;  // query tiles [it0, it1) of chunk ic
 };
 __device__ __forceinline__ Unit unit_of(long long s0, const Params& p) {
   Unit u;
   long long x = s0 / p.N;
   u.n0 = (int)(s0 - x * p.N);
+  u.ic = (int)(x % p.nIC);
+  x /= p.nIC;
   u.jt = (int)(x % p.nKT);
   x /= p.nKT;
   u.h = (int)(x % p.H);
   u.ob = (int)(x / p.H);
+  u.it0 = u.ic * p.nQC;
+  u.it1 = min(u.it0 + p.nQC, p.nQT);
   return u;
 }
 
@@ -140,6 +146,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
                const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmdO,
                const __grid_constant__ CUtensorMap tmB2, const __grid_constant__ CUtensorMap tmdQ,
+               const __grid_constant__ CUtensorMap tmdK, const __grid_constant__ CUtensorMap tmdV,
                const Params p) {
   using C = Cfg<D>;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -152,7 +159,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint8_t* sP = sV + C::kKStages * C::kTileK;                  // [2] P tiles (bf16, SW128)
   uint8_t* sdS = sP + 2 * C::kPdsTile;                         // [2] dS tiles
   uint8_t* sBias = sdS + 2 * C::kPdsTile;                      // [nQT] bias strip tiles
-  float* sDq = (float*)(sBias + (size_t)p.nQT * C::kBiasTile);  // [2] dQ staging (fp32 128 x D)
+  float* sDq = (float*)(sBias + (size_t)p.nQC * C::kBiasTile);  // [2] dQ staging (fp32 128 x D)
   uint8_t* sAaug = (uint8_t*)(sDq + 2 * kBM * D);              // 128 x 16 (1/scale split), SW32
   uint8_t* sBaug = sAaug + kAugA;                              // [KS] 64 x 16 (bias1 per key), SW32
   float* sLse = (float*)(sBaug + C::kKStages * kAugB);         // [QS][128] lse * log2e
@@ -227,9 +234,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int plane = u.ob * p.H + u.h;
         if (p.has_bias2) {
           ptx::mbar_wait_spin(bias_empty, bph ^ 1);
-          ptx::mbar_expect_tx(bias_full, p.nQT * C::kBiasTile);
-          for (int it = 0; it < p.nQT; ++it)
-            ptx::tma_load_3d(sBias + (size_t)it * C::kBiasTile, &tmB2, bias_full, u.jt * kBN, it * kBM, plane);
+          ptx::mbar_expect_tx(bias_full, (u.it1 - u.it0) * C::kBiasTile);
+          for (int it = u.it0; it < u.it1; ++it)
+            ptx::tma_load_3d(sBias + (size_t)(it - u.it0) * C::kBiasTile, &tmB2, bias_full, u.jt * kBN, it * kBM, plane);
           bph ^= 1;
         }
         int n = u.n0;
@@ -246,7 +253,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             bulk_g2s(ptx::smem_u32(sB1 + ks * 64), (const uint16_t*)p.bias1 + (size_t)b * p.L + u.jt * kBN, b1bytes,
                      &k_full[ks]);
           if (++ks == C::kKStages) { ks = 0; kph ^= 1; }
-          for (int it = 0; it < p.nQT; ++it) {
+          for (int it = u.it0; it < u.it1; ++it) {
             ptx::mbar_wait_spin(&q_empty[qs], qph ^ 1);
             trace(p, kTbProdQ, pstep++);
             ptx::mbar_expect_tx(&q_full[qs], 2 * C::kTileQ + 2 * kBM * 4);
@@ -280,10 +287,11 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint32_t step = 0, rows = 0;
     for (long long s0 = W.t0; s0 < W.t1; s0 = W.seg_end(s0)) {
       const int cnt = (int)(W.seg_end(s0) - s0);
+      const Unit u = unit_of(s0, p);
       for (int a = 0; a < cnt; ++a) {
-        for (int it = 0; it < p.nQT; ++it) {
+        for (int it = u.it0; it < u.it1; ++it) {
           const uint32_t sb = step & 1, ph = (step >> 1) & 1;
-          const bool first = it == 0, last = it == p.nQT - 1;
+          const bool first = it == u.it0, last = it == u.it1 - 1;
           ptx::mbar_wait_spin(&pds_full[sb], ph);
           if (first) {  // first q-tile of a row overwrites dK/dV: previous row must be read out
             ptx::mbar_wait_spin(kv_free, (rows & 1) ^ 1);
@@ -370,7 +378,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         const uint32_t kA = k0 + ks * (C::kTileK >> 4);
         const uint32_t vA = v0 + ks * (C::kTileK >> 4);
         const uint32_t bA = aB0 + ks * (kAugB >> 4);
-        for (int it = 0; it < p.nQT; ++it) {
+        for (int it = u.it0; it < u.it1; ++it) {
           const uint32_t sb = step & 1;
           ptx::mbar_wait_spin(&q_full[qs], qph);
           if (lane == 0) trace(p, kTbQFull, step);
@@ -421,11 +429,11 @@ __global__ void __launch_bounds__(kThreads, 1)
         uint32_t z[16];
 #pragma unroll
         for (int k = 0; k < 16; ++k) z[k] = 0u;
-        for (int it = 0; it < p.nQT; ++it) ptx::tmem_st16(tmem + lane_off + kStripCol + it * 64 + col, z);
+        for (int it = u.it0; it < u.it1; ++it) ptx::tmem_st16(tmem + lane_off + kStripCol + (it - u.it0) * 64 + col, z);
       }
       if (p.has_bias2) ptx::mbar_wait(bias_full, bph);
       for (int a = 0; a < cnt; ++a) {
-        for (int it = 0; it < p.nQT; ++it) {
+        for (int it = u.it0; it < u.it1; ++it) {
           const uint32_t sb = step & 1, ph = (step >> 1) & 1;
           ptx::mbar_wait(&q_full[qs], qph);
           const float lse2 = ptx::lds_f32(ptx::smem_u32(sLse + qs * kBM + r));
@@ -437,7 +445,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           ptx::mbar_wait(&pds_free[sb], ph ^ 1);  // P/dS buffer sb: MMAs of step-2 done
           ptx::tc_fence_after();
           // all loads of the step in flight together: S, dP, the strip (TMEM) and the bias2 row (smem)
-          const uint32_t sa = tmem + lane_off + kStripCol + it * 64 + col;
+          const uint32_t sa = tmem + lane_off + kStripCol + (it - u.it0) * 64 + col;
           uint32_t sv[16], dp[16], acc[16];
           ptx::tmem_ld16(tmem + lane_off + sb * 128 + col, sv);
           ptx::tmem_ld16(tmem + lane_off + sb * 128 + 64 + col, dp);
@@ -446,7 +454,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             ptx::tmem_ld16(sa, acc);
           }
           uint4 braw[2] = {make_uint4(0u, 0u, 0u, 0u), make_uint4(0u, 0u, 0u, 0u)};
-          const uint32_t bt = ptx::smem_u32(sBias + (size_t)it * C::kBiasTile) + r * 128;
+          const uint32_t bt = ptx::smem_u32(sBias + (size_t)(it - u.it0) * C::kBiasTile) + r * 128;
           if (p.has_bias2) {
             braw[0] = lds128(bt + ((uint32_t)((2 * wg) << 4) ^ r7));
             braw[1] = lds128(bt + ((uint32_t)((2 * wg + 1) << 4) ^ r7));
@@ -496,10 +504,10 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (p.dbias2) {
         ptx::tmem_st_wait();
         const int j0 = u.jt * kBN + (int)col;
-        for (int it = 0; it < p.nQT; ++it) {
+        for (int it = u.it0; it < u.it1; ++it) {
           const int i = it * kBM + r;
           uint32_t st[16];
-          ptx::tmem_ld16(tmem + lane_off + kStripCol + it * 64 + col, st);
+          ptx::tmem_ld16(tmem + lane_off + kStripCol + (it - u.it0) * 64 + col, st);
           ptx::tmem_ld_wait();
           if (i < p.L) {
             float* dst = p.dbias2 + (((size_t)u.ob * p.H + u.h) * p.L + i) * p.L + j0;
@@ -531,7 +539,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       int n = u.n0;
       for (int a = 0; a < cnt; ++a, ++n) {
         const int b = u.ob * p.N + n;
-        for (int it = 0; it < p.nQT; ++it) {
+        for (int it = u.it0; it < u.it1; ++it) {
           // ---- dQ partial: TMEM -> staging (fp32, swizzled rows) -> TMA reduce-add into dQacc
           ptx::mbar_wait(dq_full, step & 1);
           if (tid_e == 0) trace(p, kTbDqSeen, step);
@@ -572,9 +580,31 @@ __global__ void __launch_bounds__(kThreads, 1)
         ptx::mbar_arrive(kv_free);
         ++rows;
         const int krow = q4 * 16 + (lane & 15);
+        const bool isk = lane < 16;
+        if (p.dkv_reduce) {
+          // this query chunk's dK / dV partial of the row: fp32 rows (dK 0-63, dV 64-127) into a staging
+          // tile, TMA reduce-add into the fp32 accumulators (scaled and converted after the kernel)
+          float* stg = sDq + (step & 1) * kBM * D;
+          if (tid_e == 0) ptx::bulk_wait_read<1>();  // the previous user of this buffer was read
+          ptx::named_bar_sync(kEpiBar, 128);
+          const uint32_t sa = ptx::smem_u32(stg) + (krow + (isk ? 0 : 64)) * (D * 4);
+#pragma unroll
+          for (int c = 0; c < D; c += 4) {
+            const uint32_t off = sa + c * 4;
+            sts128(off ^ (((off >> 7) & kDqSwzMask) << 4), make_uint4(v[c], v[c + 1], v[c + 2], v[c + 3]));
+          }
+          ptx::fence_proxy_async_smem();
+          ptx::named_bar_sync(kEpiBar, 128);
+          if (tid_e == 0) {
+            ptx::tma_reduce_add_4d(&tmdK, stg, 0, u.h, u.jt * kBN, b);
+            ptx::tma_reduce_add_4d(&tmdV, stg + 64 * D, 0, u.h, u.jt * kBN, b);
+            ptx::bulk_commit();
+            ptx::bulk_wait_read<0>();  // the buffer is the next dQ step's
+          }
+          continue;
+        }
         const int j = u.jt * kBN + krow;
         if (j < p.L) {
-          const bool isk = lane < 16;
           const float sc = isk ? p.scale : 1.f;
           uint32_t ow[D / 2];
 #pragma unroll

@@ -182,15 +182,21 @@ evo_status launch_fwd(const evo_attn_desc* d, const Shape& s, const void* q, con
 
 // ---------------------------------------------------------------------------------- backward
 struct BwdScratch {
-  size_t dq, lse2, delta, total;
+  size_t dq, dk, dv, lse2, delta, total;  // dk/dv: fp32 accumulators, only when L spans several query chunks
 };
+constexpr int kBwdChunk = 3;  // query tiles per backward unit: its dBias2 strip (3 x 64 TMEM columns) fits
+int bwd_nqt(const evo_attn_desc* d) { return (int)((d->L + bk::kBM - 1) / bk::kBM); }
+int bwd_nic(const evo_attn_desc* d) { return (bwd_nqt(d) + kBwdChunk - 1) / kBwdChunk; }
 size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
 BwdScratch bwd_scratch_layout(const evo_attn_desc* d) {
   BwdScratch w{};
   const size_t B = (size_t)d->Bo * d->N;
   const size_t Lp = (size_t)((d->L + bk::kBM - 1) / bk::kBM) * bk::kBM;
+  const size_t acc = align256(B * d->L * d->H * d->D * 4);
   w.dq = 0;
-  w.lse2 = align256(B * d->L * d->H * d->D * 4);
+  w.dk = acc;
+  w.dv = w.dk + (bwd_nic(d) > 1 ? acc : 0);
+  w.lse2 = w.dv + (bwd_nic(d) > 1 ? acc : 0);
   w.delta = w.lse2 + align256(B * d->H * Lp * 4);
   w.total = w.delta + align256(B * d->H * Lp * 4);
   return w;
@@ -218,8 +224,18 @@ evo_status launch_bwd(const evo_attn_desc* d, const Shape& s, const void* dout, 
   float* dqacc = (float*)(ws + w.dq);
   float* lse2 = (float*)(ws + w.lse2);
   float* delta_p = (float*)(ws + w.delta);
-  CUtensorMap tq, tk, tv, tdo, tb, tdq;
+  CUtensorMap tq, tk, tv, tdo, tb, tdq, tdk, tdv;
   memset(&tb, 0, sizeof(tb));
+  const bool dkv_reduce = bwd_nic(d) > 1;
+  float* dkacc = (float*)(ws + w.dk);
+  float* dvacc = (float*)(ws + w.dv);
+  if (dkv_reduce) {
+    if (!map_bl_hd(&tdk, dkacc, s, bk::kBN, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, err) ||
+        !map_bl_hd(&tdv, dvacc, s, bk::kBN, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, err))
+      return EVO_ERR_CUDA;
+  } else {
+    tdk = tdv = tb;
+  }
   if (!map_bl_hd(&tq, q, s, bk::kBM, dt, 2, err) || !map_bl_hd(&tk, k, s, bk::kBN, dt, 2, err) ||
       !map_bl_hd(&tv, v, s, bk::kBN, dt, 2, err) || !map_bl_hd(&tdo, dout, s, bk::kBM, dt, 2, err) ||
       !map_bl_hd(&tdq, dqacc, s, bk::kBM, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, err))
@@ -229,7 +245,10 @@ evo_status launch_bwd(const evo_attn_desc* d, const Shape& s, const void* dout, 
   p.B = s.B; p.N = s.N; p.L = s.L; p.H = s.H; p.Bo = (int)d->Bo;
   p.nQT = (s.L + bk::kBM - 1) / bk::kBM;
   p.nKT = (s.L + bk::kBN - 1) / bk::kBN;
-  p.total = (long long)p.Bo * p.H * p.nKT * p.N;
+  p.nQC = std::min(p.nQT, kBwdChunk);
+  p.nIC = bwd_nic(d);
+  p.total = (long long)p.Bo * p.H * p.nKT * p.nIC * p.N;
+  p.dkv_reduce = dkv_reduce ? 1 : 0;
   p.scale = s.scale;
   p.scale_log2 = s.scale_log2;
   p.bias1 = s.bias1;
@@ -244,14 +263,14 @@ evo_status launch_bwd(const evo_attn_desc* d, const Shape& s, const void* dout, 
   // 16-bit two-term split of 1/scale, B_aug rows the bias1 value of each key.
   p.aug = (s.bias1 != nullptr || s.L % bk::kBN != 0) ? 1 : 0;
   p.aug_c = aug_split(1.0 / (double)s.scale, F16);
-  const size_t smem = bwd_smem_bytes<D>(p.nQT);
+  const size_t smem = bwd_smem_bytes<D>(p.nQC);
   if (smem > kMaxSmem) {
     *err = "backward shared-memory budget exceeded";
     return EVO_ERR_UNSUPPORTED;
   }
   const int Lp = p.nQT * bk::kBM;
   const long long prow = (long long)s.B * s.H;
-  cudaMemsetAsync(dqacc, 0, (size_t)s.B * s.L * s.H * D * 4, st);
+  cudaMemsetAsync(dqacc, 0, w.lse2, st);  // dQ (and dK, dV when chunked) fp32 accumulators
   using T = typename std::conditional<F16, __half, __nv_bfloat16>::type;
   if (delta) {  // delta supplied by the caller: only pad
     bk::pad_rows_kernel<<<(unsigned)std::min<long long>((prow * Lp + 255) / 256, 148 * 16), 256, 0, st>>>(
@@ -264,7 +283,7 @@ evo_status launch_bwd(const evo_attn_desc* d, const Shape& s, const void* dout, 
   auto kern = bk::bwd_kernel<D, F16>;
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   const int G = sm_count();
-  const long long units = (long long)p.Bo * p.H * p.nKT;
+  const long long units = (long long)p.Bo * p.H * p.nKT * p.nIC;
   long long grid = std::min<long long>(p.total, G);
   p.aligned = 0;
   p.split = 1;
@@ -273,12 +292,17 @@ evo_status launch_bwd(const evo_attn_desc* d, const Shape& s, const void* dout, 
     p.aligned = 1;
     grid = units * p.split;
   }
-  kern<<<(unsigned)grid, bk::kThreads, smem, st>>>(tq, tk, tv, tdo, tb, tdq, p);
+  kern<<<(unsigned)grid, bk::kThreads, smem, st>>>(tq, tk, tv, tdo, tb, tdq, tdk, tdv, p);
   ++*launches;
   const size_t n = (size_t)s.B * s.L * s.H * D;
-  bk::dq_convert_kernel<T><<<(unsigned)std::min<size_t>((n / 4 + 255) / 256, 148 * 32), 256, 0, st>>>(dqacc, (T*)dq, n,
-                                                                                                 s.scale);
+  const unsigned cg = (unsigned)std::min<size_t>((n / 4 + 255) / 256, 148 * 32);
+  bk::dq_convert_kernel<T><<<cg, 256, 0, st>>>(dqacc, (T*)dq, n, s.scale);
   ++*launches;
+  if (dkv_reduce) {  // dK = scale * dK_acc, dV = dV_acc
+    bk::dq_convert_kernel<T><<<cg, 256, 0, st>>>(dkacc, (T*)dk, n, s.scale);
+    bk::dq_convert_kernel<T><<<cg, 256, 0, st>>>(dvacc, (T*)dv, n, 1.f);
+    *launches += 2;
+  }
   return EVO_OK;
 }
 
@@ -302,11 +326,11 @@ bool device_supported() {
 size_t fwd_scratch_bytes(const evo_attn_desc*) { return 0; }
 size_t bwd_scratch_bytes(const evo_attn_desc* d) { return bwd_scratch_layout(d).total; }
 
-// tcgen05 backward: 16-bit inputs, D in {16, 32}, L % 8 == 0 (16B-aligned rows for the bulk copies)
-// and L <= 384 (the dBias2 strip of all query tiles must fit in TMEM next to S/dP, dQ, dK|dV).
+// tcgen05 backward: 16-bit inputs, D in {16, 32}, L % 8 == 0 (16B-aligned rows for the bulk copies).
+// L > 384 splits the query axis into chunks of 3 tiles (a chunk's dBias2 strip fits in TMEM next to
+// S/dP, dQ, dK|dV) and reduces dK/dV over the chunks in fp32.
 bool bwd_available(const evo_attn_desc* d) {
-  return d->dtype != EVO_F32 && (d->D == 16 || d->D == 32) && d->L % 8 == 0 && d->L <= 3 * bk::kBM &&
-         device_supported();
+  return d->dtype != EVO_F32 && (d->D == 16 || d->D == 32) && d->L % 8 == 0 && device_supported();
 }
 
 evo_status bwd(const evo_attn_desc* d, const Shape& s, const void* dout, const void* q, const void* k, const void* v,
