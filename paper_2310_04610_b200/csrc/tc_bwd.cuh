@@ -141,7 +141,7 @@ __device__ __forceinline__ void red_v4(float* gaddr, float a, float b, float c, 
   asm volatile("red.global.add.v4.f32 [%0], {%1,%2,%3,%4};" ::"l"(gaddr), "f"(a), "f"(b), "f"(c), "f"(d) : "memory");
 }
 
-template <int D, bool F16>
+template <int D, bool F16, bool CH>  // CH: the query axis is split into chunks (L > 384)
 __global__ void __launch_bounds__(kThreads, 1)
     bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
                const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmdO,
@@ -233,17 +233,17 @@ __global__ void __launch_bounds__(kThreads, 1)
         const Unit u = unit_of(s0, p);
         const int plane = u.ob * p.H + u.h;
         if (p.has_bias2) {
-          ptx::mbar_wait_spin(bias_empty, bph ^ 1);
-          ptx::mbar_expect_tx(bias_full, (u.it1 - u.it0) * C::kBiasTile);
-          for (int it = u.it0; it < u.it1; ++it)
-            ptx::tma_load_3d(sBias + (size_t)(it - u.it0) * C::kBiasTile, &tmB2, bias_full, u.jt * kBN, it * kBM, plane);
+          ptx::mbar_wait(bias_empty, bph ^ 1);
+          ptx::mbar_expect_tx(bias_full, ((CH ? u.it1 : p.nQT) - (CH ? u.it0 : 0)) * C::kBiasTile);
+          for (int it = (CH ? u.it0 : 0); it < (CH ? u.it1 : p.nQT); ++it)
+            ptx::tma_load_3d(sBias + (size_t)(it - (CH ? u.it0 : 0)) * C::kBiasTile, &tmB2, bias_full, u.jt * kBN, it * kBM, plane);
           bph ^= 1;
         }
         int n = u.n0;
         for (int a = 0; a < cnt; ++a, ++n) {
           const int b = u.ob * p.N + n;
           // K, V (and the bias1 chunk) of this row's key tile
-          ptx::mbar_wait_spin(&k_empty[ks], kph ^ 1);
+          ptx::mbar_wait(&k_empty[ks], kph ^ 1);
           const int nk = min(kBN, p.L - u.jt * kBN);  // keys of this tile (multiple of 8)
           const uint32_t b1bytes = p.bias1 ? (uint32_t)nk * 2 : 0u;
           ptx::mbar_expect_tx(&k_full[ks], 2 * C::kTileK + b1bytes);
@@ -253,8 +253,8 @@ __global__ void __launch_bounds__(kThreads, 1)
             bulk_g2s(ptx::smem_u32(sB1 + ks * 64), (const uint16_t*)p.bias1 + (size_t)b * p.L + u.jt * kBN, b1bytes,
                      &k_full[ks]);
           if (++ks == C::kKStages) { ks = 0; kph ^= 1; }
-          for (int it = u.it0; it < u.it1; ++it) {
-            ptx::mbar_wait_spin(&q_empty[qs], qph ^ 1);
+          for (int it = (CH ? u.it0 : 0); it < (CH ? u.it1 : p.nQT); ++it) {
+            ptx::mbar_wait(&q_empty[qs], qph ^ 1);
             trace(p, kTbProdQ, pstep++);
             ptx::mbar_expect_tx(&q_full[qs], 2 * C::kTileQ + 2 * kBM * 4);
             ptx::tma_load_4d(sQ + qs * C::kTileQ, &tmQ, &q_full[qs], 0, u.h, it * kBM, b);
@@ -289,9 +289,9 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int cnt = (int)(W.seg_end(s0) - s0);
       const Unit u = unit_of(s0, p);
       for (int a = 0; a < cnt; ++a) {
-        for (int it = u.it0; it < u.it1; ++it) {
+        for (int it = (CH ? u.it0 : 0); it < (CH ? u.it1 : p.nQT); ++it) {
           const uint32_t sb = step & 1, ph = (step >> 1) & 1;
-          const bool first = it == u.it0, last = it == u.it1 - 1;
+          const bool first = it == (CH ? u.it0 : 0), last = it == (CH ? u.it1 : p.nQT) - 1;
           ptx::mbar_wait_spin(&pds_full[sb], ph);
           if (first) {  // first q-tile of a row overwrites dK/dV: previous row must be read out
             ptx::mbar_wait_spin(kv_free, (rows & 1) ^ 1);
@@ -351,7 +351,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int cnt = (int)(W.seg_end(s0) - s0);
       const Unit u = unit_of(s0, p);
       for (int a = 0; a < cnt; ++a) {
-        ptx::mbar_wait_spin(&k_full[ks], kph);
+        ptx::mbar_wait(&k_full[ks], kph);
         if (p.aug) {
           // B_aug row j = (b1[j], b1[j] or 0 if non-finite) for keys < L, (-inf, 0) past L; 2 rows per lane
 #pragma unroll
@@ -378,11 +378,11 @@ __global__ void __launch_bounds__(kThreads, 1)
         const uint32_t kA = k0 + ks * (C::kTileK >> 4);
         const uint32_t vA = v0 + ks * (C::kTileK >> 4);
         const uint32_t bA = aB0 + ks * (kAugB >> 4);
-        for (int it = u.it0; it < u.it1; ++it) {
+        for (int it = (CH ? u.it0 : 0); it < (CH ? u.it1 : p.nQT); ++it) {
           const uint32_t sb = step & 1;
-          ptx::mbar_wait_spin(&q_full[qs], qph);
+          ptx::mbar_wait(&q_full[qs], qph);
           if (lane == 0) trace(p, kTbQFull, step);
-          ptx::mbar_wait_spin(&s_free[sb], ((step >> 1) & 1) ^ 1);
+          ptx::mbar_wait(&s_free[sb], ((step >> 1) & 1) ^ 1);
           ptx::tc_fence_after();
           const uint32_t qA = q0 + qs * (C::kTileQ >> 4);
           const uint32_t doA = do0 + qs * (C::kTileQ >> 4);
@@ -400,7 +400,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
           __syncwarp();
           if (p.trace && blockIdx.x == 0 && step - kTrFirst < 64u) {  // bring-up: S completion time
-            ptx::mbar_wait_spin(&s_full[sb], (step >> 1) & 1);
+            ptx::mbar_wait(&s_full[sb], (step >> 1) & 1);
             if (lane == 0) trace(p, kTbLoopTop, step);
           }
           ++step;
@@ -429,11 +429,11 @@ __global__ void __launch_bounds__(kThreads, 1)
         uint32_t z[16];
 #pragma unroll
         for (int k = 0; k < 16; ++k) z[k] = 0u;
-        for (int it = u.it0; it < u.it1; ++it) ptx::tmem_st16(tmem + lane_off + kStripCol + (it - u.it0) * 64 + col, z);
+        for (int it = (CH ? u.it0 : 0); it < (CH ? u.it1 : p.nQT); ++it) ptx::tmem_st16(tmem + lane_off + kStripCol + (it - (CH ? u.it0 : 0)) * 64 + col, z);
       }
       if (p.has_bias2) ptx::mbar_wait(bias_full, bph);
       for (int a = 0; a < cnt; ++a) {
-        for (int it = u.it0; it < u.it1; ++it) {
+        for (int it = (CH ? u.it0 : 0); it < (CH ? u.it1 : p.nQT); ++it) {
           const uint32_t sb = step & 1, ph = (step >> 1) & 1;
           ptx::mbar_wait(&q_full[qs], qph);
           const float lse2 = ptx::lds_f32(ptx::smem_u32(sLse + qs * kBM + r));
@@ -445,7 +445,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           ptx::mbar_wait(&pds_free[sb], ph ^ 1);  // P/dS buffer sb: MMAs of step-2 done
           ptx::tc_fence_after();
           // all loads of the step in flight together: S, dP, the strip (TMEM) and the bias2 row (smem)
-          const uint32_t sa = tmem + lane_off + kStripCol + (it - u.it0) * 64 + col;
+          const uint32_t sa = tmem + lane_off + kStripCol + (it - (CH ? u.it0 : 0)) * 64 + col;
           uint32_t sv[16], dp[16], acc[16];
           ptx::tmem_ld16(tmem + lane_off + sb * 128 + col, sv);
           ptx::tmem_ld16(tmem + lane_off + sb * 128 + 64 + col, dp);
@@ -454,7 +454,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             ptx::tmem_ld16(sa, acc);
           }
           uint4 braw[2] = {make_uint4(0u, 0u, 0u, 0u), make_uint4(0u, 0u, 0u, 0u)};
-          const uint32_t bt = ptx::smem_u32(sBias + (size_t)(it - u.it0) * C::kBiasTile) + r * 128;
+          const uint32_t bt = ptx::smem_u32(sBias + (size_t)(it - (CH ? u.it0 : 0)) * C::kBiasTile) + r * 128;
           if (p.has_bias2) {
             braw[0] = lds128(bt + ((uint32_t)((2 * wg) << 4) ^ r7));
             braw[1] = lds128(bt + ((uint32_t)((2 * wg + 1) << 4) ^ r7));
@@ -504,10 +504,10 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (p.dbias2) {
         ptx::tmem_st_wait();
         const int j0 = u.jt * kBN + (int)col;
-        for (int it = u.it0; it < u.it1; ++it) {
+        for (int it = (CH ? u.it0 : 0); it < (CH ? u.it1 : p.nQT); ++it) {
           const int i = it * kBM + r;
           uint32_t st[16];
-          ptx::tmem_ld16(tmem + lane_off + kStripCol + (it - u.it0) * 64 + col, st);
+          ptx::tmem_ld16(tmem + lane_off + kStripCol + (it - (CH ? u.it0 : 0)) * 64 + col, st);
           ptx::tmem_ld_wait();
           if (i < p.L) {
             float* dst = p.dbias2 + (((size_t)u.ob * p.H + u.h) * p.L + i) * p.L + j0;
@@ -539,7 +539,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       int n = u.n0;
       for (int a = 0; a < cnt; ++a, ++n) {
         const int b = u.ob * p.N + n;
-        for (int it = u.it0; it < u.it1; ++it) {
+        for (int it = (CH ? u.it0 : 0); it < (CH ? u.it1 : p.nQT); ++it) {
           // ---- dQ partial: TMEM -> staging (fp32, swizzled rows) -> TMA reduce-add into dQacc
           ptx::mbar_wait(dq_full, step & 1);
           if (tid_e == 0) trace(p, kTbDqSeen, step);
@@ -581,7 +581,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         ++rows;
         const int krow = q4 * 16 + (lane & 15);
         const bool isk = lane < 16;
-        if (p.dkv_reduce) {
+        if (CH && p.dkv_reduce) {
           // this query chunk's dK / dV partial of the row: fp32 rows (dK 0-63, dV 64-127) into a staging
           // tile, TMA reduce-add into the fp32 accumulators (scaled and converted after the kernel)
           float* stg = sDq + (step & 1) * kBM * D;

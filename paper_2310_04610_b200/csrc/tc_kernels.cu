@@ -280,7 +280,7 @@ evo_status launch_bwd(const evo_attn_desc* d, const Shape& s, const void* dout, 
         (const T*)dout, (const T*)o, lse, lse2, delta_p, s.B, s.L, s.H, Lp);
   }
   ++*launches;
-  auto kern = bk::bwd_kernel<D, F16>;
+  auto kern = dkv_reduce ? bk::bwd_kernel<D, F16, true> : bk::bwd_kernel<D, F16, false>;
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   const int G = sm_count();
   const long long units = (long long)p.Bo * p.H * p.nKT * p.nIC;
