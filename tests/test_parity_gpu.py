@@ -124,3 +124,33 @@ def test_validation_errors_map_to_taxonomy():
         E.evoformer_attention_forward(q, q, q, bias2=torch.zeros(1, 1, 2, 8, 7, dtype=torch.bfloat16, device="cuda"))
     with pytest.raises(E.NumericError):
         E.evoformer_attention_forward(q, q, q, scale=float("nan"))
+
+
+def _bwd_launches(shape, dtype="bf16"):
+    import paper_2310_04610_b200 as E
+
+    q, k, v, do, b1, b2 = make_inputs(*shape, dtype=dtype, seed=5)
+    t = lambda a: torch.tensor(a, dtype=TD[dtype], device="cuda")
+    o, lse = E.evoformer_attention_forward(t(q), t(k), t(v), t(b1), t(b2))
+    E.evoformer_attention_backward(t(do), t(q), t(k), t(v), o, lse, t(b1), t(b2))
+    torch.cuda.synchronize()
+    return E.last_launch_count()
+
+
+@pytest.mark.parametrize("shape", [(1, 2, 640, 2, 32), (1, 1, 904, 1, 32)])
+def test_tc_backward_query_chunks(shape):
+    # L > 384: the tcgen05 backward splits the query axis into chunks of 3 tiles (the chunk's dBias2
+    # strip fits in TMEM) and reduces dK/dV over the chunks in fp32; 904 also has ragged last tiles
+    check(shape, "bf16")
+    assert _bwd_launches(shape) == 5  # prep, main, dQ/dK/dV conversions: the chunked tcgen05 path ran
+
+
+def test_tc_backward_d16_and_f16():
+    check((1, 3, 96, 2, 16), "bf16")
+    check((1, 3, 96, 2, 32), "f16")
+    assert _bwd_launches((1, 3, 96, 2, 32), "f16") == 3  # prep, main, dQ conversion (tcgen05)
+
+
+def test_tc_backward_many_rows_per_cta():
+    # rows well beyond one per SM: persistent walk over units and row ranges, strip flushes per unit
+    check((1, 300, 128, 1, 32), "bf16")
