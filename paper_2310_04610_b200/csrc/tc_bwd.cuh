@@ -219,6 +219,10 @@ __global__ void __launch_bounds__(kThreads, 1)
   __syncthreads();
   ptx::tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  // launched as a programmatic dependent of the preamble: the prologue above overlapped its tail;
+  // lse2 / delta / the zeroed accumulators are read below
+  ptx::pdl_wait();
+  ptx::pdl_launch_dependents();
 
   if (warp == 0) {
     if (ptx::elect_one()) {
@@ -632,7 +636,11 @@ __global__ void __launch_bounds__(kThreads, 1)
 // Thread per (b, i, h): D contiguous elements of dO and O, 16-byte loads.
 template <int D, typename T>
 __global__ void prep_kernel(const T* __restrict__ dout, const T* __restrict__ o, const float* __restrict__ lse,
-                            float* __restrict__ lse2, float* __restrict__ delta_p, int B, int L, int H, int Lp) {
+                            float* __restrict__ lse2, float* __restrict__ delta_p, int B, int L, int H, int Lp,
+                            float4* __restrict__ zero, long long nzero4) {
+  ptx::pdl_launch_dependents();
+  for (long long x = blockIdx.x * (long long)blockDim.x + threadIdx.x; x < nzero4; x += (long long)gridDim.x * blockDim.x)
+    zero[x] = make_float4(0.f, 0.f, 0.f, 0.f);  // fp32 gradient accumulators of the main kernel
   const long long n = (long long)B * Lp * H;
   for (long long x = blockIdx.x * (long long)blockDim.x + threadIdx.x; x < n; x += (long long)gridDim.x * blockDim.x) {
     const int h = (int)(x % H);
@@ -663,7 +671,11 @@ __global__ void prep_kernel(const T* __restrict__ dout, const T* __restrict__ o,
 
 // lse2 / delta padded to whole 128-row tiles: lse2 = lse * log2e (+inf past L), delta (0 past L)
 __global__ void pad_rows_kernel(const float* __restrict__ lse, const float* __restrict__ delta, float* __restrict__ lse2,
-                                float* __restrict__ delta_p, int L, int Lp, long long rows) {
+                                float* __restrict__ delta_p, int L, int Lp, long long rows, float4* __restrict__ zero,
+                                long long nzero4) {
+  ptx::pdl_launch_dependents();
+  for (long long x = blockIdx.x * (long long)blockDim.x + threadIdx.x; x < nzero4; x += (long long)gridDim.x * blockDim.x)
+    zero[x] = make_float4(0.f, 0.f, 0.f, 0.f);
   const long long n = rows * Lp;
   for (long long x = blockIdx.x * (long long)blockDim.x + threadIdx.x; x < n; x += (long long)gridDim.x * blockDim.x) {
     const long long row = x / Lp;
@@ -677,6 +689,8 @@ __global__ void pad_rows_kernel(const float* __restrict__ lse, const float* __re
 // dQ (bf16/f16) = scale * dQacc (fp32)
 template <typename T>
 __global__ void dq_convert_kernel(const float* __restrict__ acc, T* __restrict__ dq, size_t n, float scale) {
+  ptx::pdl_wait();  // programmatic dependent of the main kernel
+  ptx::pdl_launch_dependents();
   for (size_t x = (blockIdx.x * (size_t)blockDim.x + threadIdx.x) * 4; x < n; x += (size_t)gridDim.x * blockDim.x * 4) {
     const float4 v = *(const float4*)(acc + x);
     dq[x] = from_f<T>(v.x * scale);

@@ -270,14 +270,16 @@ evo_status launch_bwd(const evo_attn_desc* d, const Shape& s, const void* dout, 
   }
   const int Lp = p.nQT * bk::kBM;
   const long long prow = (long long)s.B * s.H;
-  cudaMemsetAsync(dqacc, 0, w.lse2, st);  // dQ (and dK, dV when chunked) fp32 accumulators
+  // the preamble also zeroes the dQ (and dK, dV when chunked) fp32 accumulators: [0, w.lse2)
+  float4* zero4 = (float4*)dqacc;
+  const long long nzero4 = (long long)(w.lse2 / 16);
   using T = typename std::conditional<F16, __half, __nv_bfloat16>::type;
   if (delta) {  // delta supplied by the caller: only pad
     bk::pad_rows_kernel<<<(unsigned)std::min<long long>((prow * Lp + 255) / 256, 148 * 16), 256, 0, st>>>(
-        lse, delta, lse2, delta_p, s.L, Lp, prow);
+        lse, delta, lse2, delta_p, s.L, Lp, prow, zero4, nzero4);
   } else {
     bk::prep_kernel<D, T><<<(unsigned)std::min<long long>((prow * Lp + 255) / 256, 148 * 32), 256, 0, st>>>(
-        (const T*)dout, (const T*)o, lse, lse2, delta_p, s.B, s.L, s.H, Lp);
+        (const T*)dout, (const T*)o, lse, lse2, delta_p, s.B, s.L, s.H, Lp, zero4, nzero4);
   }
   ++*launches;
   auto kern = dkv_reduce ? bk::bwd_kernel<D, F16, true> : bk::bwd_kernel<D, F16, false>;
@@ -292,16 +294,39 @@ evo_status launch_bwd(const evo_attn_desc* d, const Shape& s, const void* dout, 
     p.aligned = 1;
     grid = units * p.split;
   }
-  kern<<<(unsigned)grid, bk::kThreads, smem, st>>>(tq, tk, tv, tdo, tb, tdq, tdk, tdv, p);
+  {  // programmatic dependent launch: the prologue overlaps the preamble's tail (pdl_wait inside)
+    cudaLaunchConfig_t cfg = {};
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.gridDim = dim3((unsigned)grid);
+    cfg.blockDim = dim3(bk::kThreads);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    cudaLaunchKernelEx(&cfg, kern, tq, tk, tv, tdo, tb, tdq, tdk, tdv, p);
+  }
   ++*launches;
   const size_t n = (size_t)s.B * s.L * s.H * D;
   const unsigned cg = (unsigned)std::min<size_t>((n / 4 + 255) / 256, 148 * 32);
-  bk::dq_convert_kernel<T><<<cg, 256, 0, st>>>(dqacc, (T*)dq, n, s.scale);
-  ++*launches;
+  auto convert = [&](const float* acc, void* out, float scale) {  // programmatic dependents of the main kernel
+    cudaLaunchConfig_t cfg = {};
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.gridDim = dim3(cg);
+    cfg.blockDim = dim3(256);
+    cfg.stream = st;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    cudaLaunchKernelEx(&cfg, bk::dq_convert_kernel<T>, acc, (T*)out, n, scale);
+    ++*launches;
+  };
+  convert(dqacc, dq, s.scale);
   if (dkv_reduce) {  // dK = scale * dK_acc, dV = dV_acc
-    bk::dq_convert_kernel<T><<<cg, 256, 0, st>>>(dkacc, (T*)dk, n, s.scale);
-    bk::dq_convert_kernel<T><<<cg, 256, 0, st>>>(dvacc, (T*)dv, n, 1.f);
-    *launches += 2;
+    convert(dkacc, dk, s.scale);
+    convert(dvacc, dv, 1.f);
   }
   return EVO_OK;
 }

@@ -164,6 +164,11 @@ __device__ __forceinline__ float lds_f32(uint32_t a) {
   return v;
 }
 
+// Programmatic dependent launch: let the next kernel in the stream start its prologue early /
+// wait until the preceding kernel's memory operations are visible.
+__device__ __forceinline__ void pdl_launch_dependents() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
 // ------------------------------------------------------------------ named barriers
 __device__ __forceinline__ void named_bar_sync(uint32_t id, uint32_t nthreads) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
