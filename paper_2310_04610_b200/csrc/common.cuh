@@ -28,6 +28,26 @@ __device__ __forceinline__ float ex2(float x) {
   return y;
 }
 
+// 2^x for a pair on the FMA pipe (relieves the MUFU pipe in softmax loops, FA4-style): x = n + f with
+// n = round(x) by the 1.5*2^23 magic add, f in [-0.5, 0.5]; 2^f by a degree-3 fit (max relative error
+// 7.7e-5, far below the bf16 rounding P receives); 2^n inserted into the exponent with one integer add.
+// Inputs are clamped at -125 so the exponent add stays in the normal range (2^-125 ~ 2.4e-38 is
+// zero for every use here: it rounds to 0 in bf16 P and vanishes in the fp32 row sums).
+__device__ __forceinline__ float2 ex2_poly2(float2 x) {
+  const float2 lo = make_float2(-125.f, -125.f);
+  x = make_float2(fmaxf(x.x, lo.x), fmaxf(x.y, lo.y));
+  const float2 magic = make_float2(12582912.f, 12582912.f);
+  const float2 t = __fadd2_rn(x, magic);                    // round(x) in the low mantissa bits
+  const float2 n = __fadd2_rn(t, make_float2(-12582912.f, -12582912.f));
+  const float2 f = __fadd2_rn(x, make_float2(-n.x, -n.y));  // [-0.5, 0.5]
+  float2 p = __ffma2_rn(f, make_float2(0.05508868f, 0.05508868f), make_float2(0.24260405f, 0.24260405f));
+  p = __ffma2_rn(f, p, make_float2(0.69327623f, 0.69327623f));
+  p = __ffma2_rn(f, p, make_float2(0.99992895f, 0.99992895f));
+  const int nx = __float_as_int(t.x) - 0x4B400000, ny = __float_as_int(t.y) - 0x4B400000;
+  return make_float2(__int_as_float(__float_as_int(p.x) + (nx << 23)),
+                     __int_as_float(__float_as_int(p.y) + (ny << 23)));
+}
+
 // Shape/stride bundle shared by every kernel. Canonical row index b in
 // [0, B) with B = Bo*N; tensors are (B, L, H, D) row-major.
 struct Shape {

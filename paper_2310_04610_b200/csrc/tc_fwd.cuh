@@ -32,6 +32,10 @@ namespace tc {
 constexpr int kBM = 128;                 // query rows per tile (UMMA M, TMEM lanes)
 constexpr int kBN = 64;                  // keys per tile (UMMA N of S)
 constexpr float kRescaleThreshold = 8.f;  // log2 units
+#ifndef EVO_FWD_POLY_EVERY
+#define EVO_FWD_POLY_EVERY 4
+#endif
+constexpr int kPolyEvery = EVO_FWD_POLY_EVERY;  // 1 pair in kPolyEvery exponentiated by polynomial (0: none)
 
 template <int D>
 struct FwdCfg {
@@ -538,8 +542,12 @@ __global__ void __launch_bounds__(FwdCfg<D>::kThreads, 1)
 #pragma unroll
           for (int k = 0; k < 32; ++k) {
             float2 t = __fadd2_rn(x[k], nb);
-            t.x = ex2(t.x);
-            t.y = ex2(t.y);
+            if (kPolyEvery > 0 && k % kPolyEvery == kPolyEvery - 1) {
+              t = ex2_poly2(t);  // every kPolyEvery-th pair on the FMA pipe, the rest on MUFU
+            } else {
+              t.x = ex2(t.x);
+              t.y = ex2(t.y);
+            }
             sum[k & 1] = __fadd2_rn(sum[k & 1], t);
             pk[k] = F16 ? ptx::pack_f16(t.x, t.y) : ptx::pack_bf16(t.x, t.y);
           }
