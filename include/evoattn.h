@@ -65,6 +65,12 @@ typedef struct {
   evo_dtype dbias_dtype; /* dtype of dbias1/dbias2 outputs: EVO_F32 = the reference's
                             UpcastF32 policy (attention_tiled.cpp:218-223), or == dtype */
   evo_path path;
+  void* dbias2_multicast; /* backward, multi-GPU: NVSwitch multicast address of a symmetric fp32
+                             dBias2 buffer (dbias2 = this rank's replica, dbias_dtype EVO_F32,
+                             accumulate_dbias = 1). The kernel adds its partial through it, so every
+                             rank's replica receives the sum of all ranks: the cross-GPU reduction
+                             happens inside the kernel. The caller zeroes all replicas and
+                             synchronises the ranks before and after the call. NULL = local only. */
 } evo_attn_desc;
 
 size_t evo_attn_fwd_workspace_size(const evo_attn_desc* desc);

@@ -221,6 +221,9 @@ evo_status evo_attn_bwd(const evo_attn_desc* d, const void* dout, const void* q,
   if (dbias2 && !d->has_bias2) return fail(EVO_ERR_VALIDATION, "dbias2 requested without bias2");
   if (accumulate_dbias && d->dbias_dtype != EVO_F32)
     return fail(EVO_ERR_VALIDATION, "accumulate_dbias requires dbias_dtype == EVO_F32");
+  if (d->dbias2_multicast && (!dbias2 || d->dbias_dtype != EVO_F32 || !accumulate_dbias))
+    return fail(EVO_ERR_VALIDATION,
+                "dbias2_multicast needs dbias2 (this rank's replica), dbias_dtype EVO_F32 and accumulate_dbias");
   const BwdWs w = bwd_layout(d);
   if (!workspace || workspace_bytes < w.total) return fail(EVO_ERR_VALIDATION, "workspace too small");
   const int path = resolve(d);
@@ -238,7 +241,10 @@ evo_status evo_attn_bwd(const evo_attn_desc* d, const void* dout, const void* q,
     if (db2) cudaMemsetAsync(db2, 0, n2 * 4, cs);
     if (db1) cudaMemsetAsync(db1, 0, n1 * 4, cs);
   }
-  if (path == EVO_PATH_TCGEN05 && evo::tc::bwd_available(d) && !dbias1) {
+  const bool tc_bwd = path == EVO_PATH_TCGEN05 && evo::tc::bwd_available(d) && !dbias1;
+  if (d->dbias2_multicast && !tc_bwd)
+    return fail(EVO_ERR_UNSUPPORTED, "the multicast dBias2 reduction needs the tcgen05 backward (16-bit, D 16/32, L % 8 == 0)");
+  if (tc_bwd) {
     // the tcgen05 preamble computes delta itself
     st = evo::tc::bwd(d, s, dout, q, k, v, o, lse, nullptr, dq, dk, dv, db1, db2, ws + w.tc, cs,
                       &g_launches, &g_err);

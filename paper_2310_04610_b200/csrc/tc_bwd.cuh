@@ -67,7 +67,8 @@ struct Params {
   void* dk;             // [B, L, H, D] (nIC == 1: written directly)
   void* dv;
   int dkv_reduce;       // nIC > 1: dK/dV partials of each query chunk reduce-add into fp32 accumulators
-  float* dbias2;        // [Bo, H, L, L] fp32 accumulator or null
+  float* dbias2;        // [Bo, H, L, L] fp32 accumulator or null (a multicast address when dbias2_mc)
+  int dbias2_mc;        // flush the dBias2 strip with multimem.red into every rank's replica
   int has_bias2;
   int aug;             // extra K-step adding bias1 / scale (bias1 present or L % 64 != 0)
   uint32_t aug_c;      // (c_lo << 16) | c_hi: 16-bit split of 1/scale
@@ -139,6 +140,13 @@ __device__ __forceinline__ float2 unpack2(uint32_t w) {
 }
 __device__ __forceinline__ void red_v4(float* gaddr, float a, float b, float c, float d) {
   asm volatile("red.global.add.v4.f32 [%0], {%1,%2,%3,%4};" ::"l"(gaddr), "f"(a), "f"(b), "f"(c), "f"(d) : "memory");
+}
+// NVLS: one add through an NVSwitch multicast address lands in every GPU's replica (the cross-GPU
+// dBias2 reduction fused into the kernel's strip flush — no separate all-reduce)
+__device__ __forceinline__ void red_v4_multimem(float* mc_addr, float a, float b, float c, float d) {
+  asm volatile("multimem.red.relaxed.sys.global.add.v4.f32 [%0], {%1,%2,%3,%4};" ::"l"(mc_addr), "f"(a), "f"(b),
+               "f"(c), "f"(d)
+               : "memory");
 }
 
 template <int D, bool F16, bool CH>  // CH: the query axis is split into chunks (L > 384)
@@ -517,12 +525,18 @@ __global__ void __launch_bounds__(kThreads, 1)
             float* dst = p.dbias2 + (((size_t)u.ob * p.H + u.h) * p.L + i) * p.L + j0;
 #pragma unroll
             for (int k = 0; k < 16; k += 4)
-              if (j0 + k < p.L)
-                red_v4(dst + k, __uint_as_float(st[k]), __uint_as_float(st[k + 1]), __uint_as_float(st[k + 2]),
-                       __uint_as_float(st[k + 3]));
+              if (j0 + k < p.L) {
+                if (p.dbias2_mc)
+                  red_v4_multimem(dst + k, __uint_as_float(st[k]), __uint_as_float(st[k + 1]),
+                                  __uint_as_float(st[k + 2]), __uint_as_float(st[k + 3]));
+                else
+                  red_v4(dst + k, __uint_as_float(st[k]), __uint_as_float(st[k + 1]), __uint_as_float(st[k + 2]),
+                         __uint_as_float(st[k + 3]));
+              }
           }
         }
       }
+      if (p.dbias2 && p.dbias2_mc) __threadfence_system();  // remote adds ordered before the ranks' barrier
       if (p.has_bias2) {
         ptx::named_bar_sync(1 + wg, 128);
         if (tid_wg == 0) ptx::mbar_arrive(bias_empty);

@@ -257,6 +257,10 @@ evo_status launch_bwd(const evo_attn_desc* d, const Shape& s, const void* dout, 
   p.dk = dk;
   p.dv = dv;
   p.dbias2 = dbias2;
+  if (d->dbias2_multicast && dbias2) {  // cross-GPU dBias2 reduction fused into the strip flush (NVLS)
+    p.dbias2 = (float*)d->dbias2_multicast;
+    p.dbias2_mc = 1;
+  }
   p.has_bias2 = s.bias2 != nullptr;
   p.trace = g_trace_bwd;
   // bias1 (and the key mask past L) enter S through one extra K=16 MMA step: A_aug rows hold a

@@ -83,7 +83,8 @@ def evoformer_attention_forward(q, k, v, bias1=None, bias2=None, scale=None, pat
 def evoformer_attention_backward(dout, q, k, v, o, lse, bias1=None, bias2=None, scale=None,
                                  need_dbias1: bool = False, need_dbias2: bool = True,
                                  dbias_dtype: Optional[torch.dtype] = torch.float32,
-                                 path: str = "auto", dbias_out: Optional[Tuple] = None):
+                                 path: str = "auto", dbias_out: Optional[Tuple] = None,
+                                 dbias2_multicast: int = 0):
     """dQ, dK, dV and the broadcast-reduced bias gradients.
 
     dbias2 is sum over the N (row) axis of dS, reduced inside the kernels, in
@@ -95,6 +96,7 @@ def evoformer_attention_backward(dout, q, k, v, o, lse, bias1=None, bias2=None, 
     if dout.shape != q.shape or o.shape != q.shape or dout.dtype != q.dtype or o.dtype != q.dtype:
         raise N.ValidationError("output and grad_output must match Q/K/V shape and dtype")
     d = make_desc(q, bias1, bias2, scale, path, dbias_dtype)
+    d.dbias2_multicast = dbias2_multicast or None  # NVSwitch multicast address of a symmetric dBias2 buffer
     if tuple(lse.shape) != (d.Bo * d.N, d.H, d.L) or lse.dtype != torch.float32:
         raise N.ValidationError(f"lse must be [B, H, L] float32, got {tuple(lse.shape)} {lse.dtype}")
     dq, dk, dv = torch.empty_like(q), torch.empty_like(q), torch.empty_like(q)
