@@ -241,7 +241,7 @@ evo_status evo_attn_bwd(const evo_attn_desc* d, const void* dout, const void* q,
     if (db2) cudaMemsetAsync(db2, 0, n2 * 4, cs);
     if (db1) cudaMemsetAsync(db1, 0, n1 * 4, cs);
   }
-  const bool tc_bwd = path == EVO_PATH_TCGEN05 && evo::tc::bwd_available(d) && !dbias1;
+  const bool tc_bwd = path == EVO_PATH_TCGEN05 && evo::tc::bwd_available(d);
   if (d->dbias2_multicast && !tc_bwd)
     return fail(EVO_ERR_UNSUPPORTED, "the multicast dBias2 reduction needs the tcgen05 backward (16-bit, D 16/32, L % 8 == 0)");
   if (tc_bwd) {

@@ -40,7 +40,9 @@ constexpr int kThreads = (kEpiWarp0 + 4) * 32;
 constexpr int kSoftThreads = 128 * kSoftWG;
 constexpr uint32_t kEpiBar = 1 + kSoftWG;               // named barrier of the epilogue WG
 constexpr int kAugA = kBM * 32, kAugB = 64 * 32;        // bias1 augmentation tiles (16 bf16 per row)
+constexpr int kOnes = 16 * 32;                           // 16 x 16 bf16 ones: the dBias1 column-sum operand
 constexpr uint32_t kStripCol = 256, kDqCol = 448, kDkvCol = 480;
+constexpr uint32_t kDb1Col = 384;  // dBias1 column sums (M=64, 16 columns) when requested: chunks of <= 2 q-tiles
 
 template <int D>
 struct Cfg {
@@ -68,6 +70,7 @@ struct Params {
   void* dv;
   int dkv_reduce;       // nIC > 1: dK/dV partials of each query chunk reduce-add into fp32 accumulators
   float* dbias2;        // [Bo, H, L, L] fp32 accumulator or null (a multicast address when dbias2_mc)
+  float* dbias1;        // [B, L] fp32 accumulator or null: dBias1[b, j] = sum_{h,i} dS (the mask-bias gradient)
   int dbias2_mc;        // flush the dBias2 strip with multimem.red into every rank's replica
   int has_bias2;
   int aug;             // extra K-step adding bias1 / scale (bias1 present or L % 64 != 0)
@@ -170,7 +173,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   float* sDq = (float*)(sBias + (size_t)p.nQC * C::kBiasTile);  // [2] dQ staging (fp32 128 x D)
   uint8_t* sAaug = (uint8_t*)(sDq + 2 * kBM * D);              // 128 x 16 (1/scale split), SW32
   uint8_t* sBaug = sAaug + kAugA;                              // [KS] 64 x 16 (bias1 per key), SW32
-  float* sLse = (float*)(sBaug + C::kKStages * kAugB);         // [QS][128] lse * log2e
+  uint8_t* sOnes = sBaug + C::kKStages * kAugB;                // 16 x 16 ones (dBias1 = dS^T 1), SW32
+  float* sLse = (float*)(sOnes + kOnes);                       // [QS][128] lse * log2e
   float* sDel = sLse + C::kQStages * kBM;                      // [QS][128] delta
   uint16_t* sB1 = (uint16_t*)(sDel + C::kQStages * kBM);       // [KS][64] bias1 chunk (raw)
   uint64_t* bars = (uint64_t*)(sB1 + C::kKStages * 64);
@@ -215,6 +219,10 @@ __global__ void __launch_bounds__(kThreads, 1)
   // A_aug: row i = (c_hi, c_lo, 0, ...): one extra K=16 step of S = Q K^T adds (c_hi + c_lo) * B_aug[j][0..1]
   // = bias1[j] / scale (two-term split of 1/scale, exact to ~2^-16). 16B chunk 0 of a 32B row sits at
   // chunk position (i >> 2) & 1 under the 32B swizzle.
+  for (int i = threadIdx.x; i < 16 * 2; i += blockDim.x) {  // ones (1.0 in bf16 / f16), layout-agnostic
+    const uint32_t one = F16 ? 0x3C003C00u : 0x3F803F80u;
+    ((uint4*)sOnes)[i] = make_uint4(one, one, one, one);
+  }
   for (int i = threadIdx.x; i < kBM; i += blockDim.x) {
     const uint32_t c = (uint32_t)((i >> 2) & 1);
     uint4* row = (uint4*)(sAaug + i * 32);
@@ -295,6 +303,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     const uint32_t p0mn = ptx::desc_lo(ptx::smem_u32(sP), 1024), ds0mn = ptx::desc_lo(ptx::smem_u32(sdS), 1024);
     const uint32_t ds0k = ptx::desc_lo(ptx::smem_u32(sdS), 16);
     const uint32_t tdKV = tmem + kDkvCol, tdQ = tmem + kDqCol;
+    const uint32_t idB1 = ptx::instr_desc(64, 16, F16, true, false);  // dBias1: MN-major dS^T, K-major ones
+    const uint64_t bOnes = ptx::desc_make(ptx::desc_lo(ptx::smem_u32(sOnes), 16), ptx::desc_hi(256, 6));
     int qs = 0, ks = 0;
     uint32_t step = 0, rows = 0;
     for (long long s0 = W.t0; s0 < W.t1; s0 = W.seg_end(s0)) {
@@ -327,6 +337,8 @@ __global__ void __launch_bounds__(kThreads, 1)
                           ptx::desc_make(doB + kk * kRow16, kHiMN), idKV, acc);  // dV (lanes 16-31 of each quadrant)
               ptx::mma_ss(tdKV, ptx::desc_make(dsA + kk * 128, kHiP), ptx::desc_make(qB + kk * kRow16, kHiMN), idKV,
                           acc);                                                  // dK (lanes 0-15)
+              if (p.dbias1)  // dBias1 partial: dS^T (keys x queries) times a ones column block
+                ptx::mma_ss(tmem + kDb1Col, ptx::desc_make(dsA + kk * 128, kHiP), bOnes, idB1, acc);
             }
 #pragma unroll
             for (int kk = 0; kk < kBN / 16; ++kk)  // dQ = dS K: K = 64 keys (+32 B in the dS rows)
@@ -593,9 +605,15 @@ __global__ void __launch_bounds__(kThreads, 1)
         uint32_t v[D];
 #pragma unroll
         for (int c0 = 0; c0 < D; c0 += 16) ptx::tmem_ld16(tmem + lane_off + kDkvCol + c0, *(uint32_t(*)[16])(&v[c0]));
+        uint32_t b1v[4];
+        if (p.dbias1) ptx::tmem_ld4(tmem + lane_off + kDb1Col, b1v);
         ptx::tmem_ld_wait();
         ptx::tc_fence_before();
         ptx::mbar_arrive(kv_free);
+        if (p.dbias1 && lane < 16) {  // lanes 0-15 of quadrant q4 hold keys q4*16 + lane (M=64 layout)
+          const int jj = u.jt * kBN + q4 * 16 + lane;
+          if (jj < p.L) atomicAdd(p.dbias1 + (size_t)b * p.L + jj, __uint_as_float(b1v[0]));
+        }
         ++rows;
         const int krow = q4 * 16 + (lane & 15);
         const bool isk = lane < 16;

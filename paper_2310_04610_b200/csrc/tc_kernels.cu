@@ -186,7 +186,12 @@ struct BwdScratch {
 };
 constexpr int kBwdChunk = 3;  // query tiles per backward unit: its dBias2 strip (3 x 64 TMEM columns) fits
 int bwd_nqt(const evo_attn_desc* d) { return (int)((d->L + bk::kBM - 1) / bk::kBM); }
-int bwd_nic(const evo_attn_desc* d) { return (bwd_nqt(d) + kBwdChunk - 1) / kBwdChunk; }
+// dBias1 needs 16 TMEM columns: its chunks hold 2 query tiles (strip 128 columns) instead of 3
+int bwd_chunk(const evo_attn_desc* d, bool db1) { return std::min(bwd_nqt(d), db1 ? 2 : kBwdChunk); }
+int bwd_nic(const evo_attn_desc* d, bool db1 = false) {
+  const int c = bwd_chunk(d, db1);
+  return (bwd_nqt(d) + c - 1) / c;
+}
 size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
 BwdScratch bwd_scratch_layout(const evo_attn_desc* d) {
   BwdScratch w{};
@@ -195,8 +200,10 @@ BwdScratch bwd_scratch_layout(const evo_attn_desc* d) {
   const size_t acc = align256(B * d->L * d->H * d->D * 4);
   w.dq = 0;
   w.dk = acc;
-  w.dv = w.dk + (bwd_nic(d) > 1 ? acc : 0);
-  w.lse2 = w.dv + (bwd_nic(d) > 1 ? acc : 0);
+  // dK/dV accumulators when the query axis may be chunked (a dBias1 request chunks by 2 tiles)
+  const bool may_chunk = bwd_nic(d, d->has_bias1 != 0) > 1;
+  w.dv = w.dk + (may_chunk ? acc : 0);
+  w.lse2 = w.dv + (may_chunk ? acc : 0);
   w.delta = w.lse2 + align256(B * d->H * Lp * 4);
   w.total = w.delta + align256(B * d->H * Lp * 4);
   return w;
@@ -208,7 +215,7 @@ size_t bwd_smem_bytes(int nQT) {
   size_t b = 1024;
   b += (size_t)C::kQStages * 2 * C::kTileQ + (size_t)C::kKStages * 2 * C::kTileK + 4 * (size_t)C::kPdsTile;
   b += (size_t)nQT * C::kBiasTile + 2 * (size_t)bk::kBM * D * 4;
-  b += (size_t)bk::kAugA + (size_t)C::kKStages * bk::kAugB;
+  b += (size_t)bk::kAugA + (size_t)C::kKStages * bk::kAugB + bk::kOnes;
   b += (size_t)C::kQStages * bk::kBM * 4 * 2 + (size_t)C::kKStages * 64 * 2;
   b += (size_t)(2 * C::kQStages + 2 * C::kKStages + 8 + 6) * 8 + 16;
   return b;
@@ -217,7 +224,8 @@ size_t bwd_smem_bytes(int nQT) {
 template <int D, bool F16>
 evo_status launch_bwd(const evo_attn_desc* d, const Shape& s, const void* dout, const void* q, const void* k,
                       const void* v, const void* o, const float* lse, const float* delta, void* dq, void* dk, void* dv,
-                      float* dbias2, void* scratch, cudaStream_t st, int* launches, std::string* err) {
+                      float* dbias1, float* dbias2, void* scratch, cudaStream_t st, int* launches,
+                      std::string* err) {
   const CUtensorMapDataType dt = F16 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT16 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16;
   const BwdScratch w = bwd_scratch_layout(d);
   char* ws = (char*)scratch;
@@ -226,7 +234,8 @@ evo_status launch_bwd(const evo_attn_desc* d, const Shape& s, const void* dout, 
   float* delta_p = (float*)(ws + w.delta);
   CUtensorMap tq, tk, tv, tdo, tb, tdq, tdk, tdv;
   memset(&tb, 0, sizeof(tb));
-  const bool dkv_reduce = bwd_nic(d) > 1;
+  const bool want_db1 = dbias1 != nullptr;
+  const bool dkv_reduce = bwd_nic(d, want_db1) > 1;
   float* dkacc = (float*)(ws + w.dk);
   float* dvacc = (float*)(ws + w.dv);
   if (dkv_reduce) {
@@ -245,8 +254,9 @@ evo_status launch_bwd(const evo_attn_desc* d, const Shape& s, const void* dout, 
   p.B = s.B; p.N = s.N; p.L = s.L; p.H = s.H; p.Bo = (int)d->Bo;
   p.nQT = (s.L + bk::kBM - 1) / bk::kBM;
   p.nKT = (s.L + bk::kBN - 1) / bk::kBN;
-  p.nQC = std::min(p.nQT, kBwdChunk);
-  p.nIC = bwd_nic(d);
+  p.nQC = bwd_chunk(d, want_db1);
+  p.nIC = bwd_nic(d, want_db1);
+  p.dbias1 = dbias1;
   p.total = (long long)p.Bo * p.H * p.nKT * p.nIC * p.N;
   p.dkv_reduce = dkv_reduce ? 1 : 0;
   p.scale = s.scale;
@@ -276,7 +286,7 @@ evo_status launch_bwd(const evo_attn_desc* d, const Shape& s, const void* dout, 
   const long long prow = (long long)s.B * s.H;
   // the preamble also zeroes the dQ (and dK, dV when chunked) fp32 accumulators: [0, w.lse2)
   float4* zero4 = (float4*)dqacc;
-  const long long nzero4 = (long long)(w.lse2 / 16);
+  const long long nzero4 = (long long)((dkv_reduce ? w.lse2 : w.dk) / 16);  // only the accumulators this call uses
   using T = typename std::conditional<F16, __half, __nv_bfloat16>::type;
   if (delta) {  // delta supplied by the caller: only pad
     bk::pad_rows_kernel<<<(unsigned)std::min<long long>((prow * Lp + 255) / 256, 148 * 16), 256, 0, st>>>(
@@ -365,16 +375,12 @@ bool bwd_available(const evo_attn_desc* d) {
 evo_status bwd(const evo_attn_desc* d, const Shape& s, const void* dout, const void* q, const void* k, const void* v,
                const void* o, const float* lse, const float* delta, void* dq, void* dk, void* dv, float* dbias1, float* dbias2,
                void* scratch, cudaStream_t st, int* launches, std::string* err) {
-  if (dbias1) {
-    *err = "tcgen05 backward does not produce dbias1";
-    return EVO_ERR_UNSUPPORTED;
-  }
   const bool f16 = d->dtype == EVO_F16;
   switch (d->D) {
-    case 16: return f16 ? launch_bwd<16, true>(d, s, dout, q, k, v, o, lse, delta, dq, dk, dv, dbias2, scratch, st, launches, err)
-                        : launch_bwd<16, false>(d, s, dout, q, k, v, o, lse, delta, dq, dk, dv, dbias2, scratch, st, launches, err);
-    case 32: return f16 ? launch_bwd<32, true>(d, s, dout, q, k, v, o, lse, delta, dq, dk, dv, dbias2, scratch, st, launches, err)
-                        : launch_bwd<32, false>(d, s, dout, q, k, v, o, lse, delta, dq, dk, dv, dbias2, scratch, st, launches, err);
+    case 16: return f16 ? launch_bwd<16, true>(d, s, dout, q, k, v, o, lse, delta, dq, dk, dv, dbias1, dbias2, scratch, st, launches, err)
+                        : launch_bwd<16, false>(d, s, dout, q, k, v, o, lse, delta, dq, dk, dv, dbias1, dbias2, scratch, st, launches, err);
+    case 32: return f16 ? launch_bwd<32, true>(d, s, dout, q, k, v, o, lse, delta, dq, dk, dv, dbias1, dbias2, scratch, st, launches, err)
+                        : launch_bwd<32, false>(d, s, dout, q, k, v, o, lse, delta, dq, dk, dv, dbias1, dbias2, scratch, st, launches, err);
     default: *err = "tcgen05 backward supports D in {16, 32}"; return EVO_ERR_UNSUPPORTED;
   }
 }

@@ -154,3 +154,10 @@ def test_tc_backward_d16_and_f16():
 def test_tc_backward_many_rows_per_cta():
     # rows well beyond one per SM: persistent walk over units and row ranges, strip flushes per unit
     check((1, 300, 128, 1, 32), "bf16")
+
+
+@pytest.mark.parametrize("shape", [(1, 4, 384, 2, 32), (2, 2, 200, 2, 32)])
+def test_tc_backward_dbias1(shape):
+    # the mask-bias gradient on the tcgen05 path: column sums of dS from an extra UMMA against a ones
+    # block (L = 384 runs in chunks of 2 query tiles to free the TMEM columns)
+    check(shape, "bf16", need_dbias1=True)
