@@ -41,8 +41,12 @@ constexpr int kSoftThreads = 128 * kSoftWG;
 constexpr uint32_t kEpiBar = 1 + kSoftWG;               // named barrier of the epilogue WG
 constexpr int kAugA = kBM * 32, kAugB = 64 * 32;        // bias1 augmentation tiles (16 bf16 per row)
 constexpr int kOnes = 16 * 32;                           // 16 x 16 bf16 ones: the dBias1 column-sum operand
+constexpr int kIdent = 16 * 32;                          // 16 x 16 identity: dBias2 strip += dS I on the tensor pipe
 constexpr uint32_t kStripCol = 256, kDqCol = 448, kDkvCol = 480;
-constexpr uint32_t kDb1Col = 384;  // dBias1 column sums (M=64, 16 columns) when requested: chunks of <= 2 q-tiles
+constexpr uint32_t kDb1Col = 384;
+#ifndef EVO_BWD_EXP
+#define EVO_BWD_EXP 0  // timing experiments only (wrong results), bit mask: 1 no dK/dV MMAs, 2 no dQ MMA, 4 no bias LDS, 8 no P/dS stores
+#endif  // dBias1 column sums (M=64, 16 columns) when requested: chunks of <= 2 q-tiles
 
 template <int D>
 struct Cfg {
@@ -174,7 +178,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint8_t* sAaug = (uint8_t*)(sDq + 2 * kBM * D);              // 128 x 16 (1/scale split), SW32
   uint8_t* sBaug = sAaug + kAugA;                              // [KS] 64 x 16 (bias1 per key), SW32
   uint8_t* sOnes = sBaug + C::kKStages * kAugB;                // 16 x 16 ones (dBias1 = dS^T 1), SW32
-  float* sLse = (float*)(sOnes + kOnes);                       // [QS][128] lse * log2e
+  uint8_t* sIdent = sOnes + kOnes;                             // 16 x 16 identity (strip += dS I), SW32
+  float* sLse = (float*)(sIdent + kIdent);                     // [QS][128] lse * log2e
   float* sDel = sLse + C::kQStages * kBM;                      // [QS][128] delta
   uint16_t* sB1 = (uint16_t*)(sDel + C::kQStages * kBM);       // [KS][64] bias1 chunk (raw)
   uint64_t* bars = (uint64_t*)(sB1 + C::kKStages * 64);
@@ -192,7 +197,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* kv_free = kv_done + 1;                  // [1] dK/dV read out
   uint64_t* bias_full = kv_free + 1;                // [1] bias strip of the unit landed
   uint64_t* bias_empty = bias_full + 1;             // [1] strip readers done (one arrival per WG)
-  uint32_t* tmem_slot = (uint32_t*)(bias_empty + 1);
+  uint64_t* strip_full = bias_empty + 1;            // [1] last dBias2 strip MMA of a unit completed
+  uint32_t* tmem_slot = (uint32_t*)(strip_full + 1);
 
   const int warp = threadIdx.x / 32;
   const int lane = threadIdx.x % 32;
@@ -214,6 +220,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     ptx::mbar_init(kv_free, 128);
     ptx::mbar_init(bias_full, 1);
     ptx::mbar_init(bias_empty, kSoftWG);
+    ptx::mbar_init(strip_full, 1);
     ptx::fence_barrier_init();
   }
   // A_aug: row i = (c_hi, c_lo, 0, ...): one extra K=16 step of S = Q K^T adds (c_hi + c_lo) * B_aug[j][0..1]
@@ -222,6 +229,15 @@ __global__ void __launch_bounds__(kThreads, 1)
   for (int i = threadIdx.x; i < 16 * 2; i += blockDim.x) {  // ones (1.0 in bf16 / f16), layout-agnostic
     const uint32_t one = F16 ? 0x3C003C00u : 0x3F803F80u;
     ((uint4*)sOnes)[i] = make_uint4(one, one, one, one);
+  }
+  for (int i = threadIdx.x; i < 16; i += blockDim.x) {  // identity row i: element i = 1 in chunk (i >> 3) ^ ((i >> 2) & 1)
+    const uint32_t one = F16 ? 0x3C00u : 0x3F80u;
+    uint32_t w[8] = {0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u};
+    w[(i & 7) >> 1] = (i & 1) ? (one << 16) : one;
+    uint4* row = (uint4*)(sIdent + i * 32);
+    const uint32_t c = (uint32_t)(i >> 3) ^ (uint32_t)((i >> 2) & 1);
+    row[c] = make_uint4(w[0], w[1], w[2], w[3]);
+    row[c ^ 1] = make_uint4(0u, 0u, 0u, 0u);
   }
   for (int i = threadIdx.x; i < kBM; i += blockDim.x) {
     const uint32_t c = (uint32_t)((i >> 2) & 1);
@@ -305,6 +321,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     const uint32_t tdKV = tmem + kDkvCol, tdQ = tmem + kDqCol;
     const uint32_t idB1 = ptx::instr_desc(64, 16, F16, true, false);  // dBias1: MN-major dS^T, K-major ones
     const uint64_t bOnes = ptx::desc_make(ptx::desc_lo(ptx::smem_u32(sOnes), 16), ptx::desc_hi(256, 6));
+    const uint32_t idStrip = ptx::instr_desc(kBM, 16, F16, false, false);  // strip block += dS block x I16
+    const uint64_t bIdent = ptx::desc_make(ptx::desc_lo(ptx::smem_u32(sIdent), 16), ptx::desc_hi(256, 6));
     int qs = 0, ks = 0;
     uint32_t step = 0, rows = 0;
     for (long long s0 = W.t0; s0 < W.t1; s0 = W.seg_end(s0)) {
@@ -329,7 +347,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           const uint32_t kB = k0n + ks * (C::kTileK >> 4);
           if (ptx::elect_one()) {
 #pragma unroll
-            for (int kk = 0; kk < kBM / 16; ++kk) {  // K = 128 queries: 16 rows per step
+            for (int kk = 0; kk < ((EVO_BWD_EXP & 1) ? 0 : kBM / 16); ++kk) {  // K = 128 queries: 16 rows per step
               // A = P^T / dS^T: MN-major SW128 (64 keys wide), 16 query rows = 2 x 8-row atoms (+2048 B)
               // B = dO / Q: MN-major (D wide), 16 query rows (+16 * 2D B)
               const uint32_t acc = (!first || kk > 0) ? 1u : 0u;
@@ -341,10 +359,19 @@ __global__ void __launch_bounds__(kThreads, 1)
                 ptx::mma_ss(tmem + kDb1Col, ptx::desc_make(dsA + kk * 128, kHiP), bOnes, idB1, acc);
             }
 #pragma unroll
-            for (int kk = 0; kk < kBN / 16; ++kk)  // dQ = dS K: K = 64 keys (+32 B in the dS rows)
+            for (int kk = 0; kk < ((EVO_BWD_EXP & 2) ? 0 : kBN / 16); ++kk)  // dQ = dS K: K = 64 keys (+32 B in the dS rows)
               ptx::mma_ss(tdQ, ptx::desc_make(dsK + kk * 2, kHiP), ptx::desc_make(kB + kk * kRow16, kHiMN), idQ,
                           kk > 0);
             ptx::tc_commit(dq_full);
+            if (p.dbias2) {
+              // dBias2 strip (this q-tile's 128 x 64 fp32 block in TMEM) += dS: four N = 16 column blocks,
+              // dS block kk (K-major, 16 keys) times a 16 x 16 identity; the unit's first row initialises
+              const uint32_t st = tmem + kStripCol + (uint32_t)(it - (CH ? u.it0 : 0)) * 64;
+#pragma unroll
+              for (int kk = 0; kk < kBN / 16; ++kk)
+                ptx::mma_ss(st + kk * 16, ptx::desc_make(dsK + kk * 2, kHiP), bIdent, idStrip, a > 0 ? 1u : 0u);
+              if (last && a == cnt - 1) ptx::tc_commit(strip_full);
+            }
             ptx::tc_commit(&pds_free[sb]);
             ptx::tc_commit(&q_empty[qs]);  // S/dP of this step completed before P/dS existed
             if (last) {
@@ -445,16 +472,10 @@ __global__ void __launch_bounds__(kThreads, 1)
     const float2 lg2 = make_float2(kLog2e, kLog2e);
     const uint32_t r7 = (uint32_t)(r & 7) << 4;
     int qs = 0; uint32_t qph = 0;
-    uint32_t step = 0, bph = 0;
+    uint32_t step = 0, bph = 0, uph = 0;
     for (long long s0 = W.t0; s0 < W.t1; s0 = W.seg_end(s0)) {
       const int cnt = (int)(W.seg_end(s0) - s0);
       const Unit u = unit_of(s0, p);
-      if (p.dbias2) {  // zero this thread's strip columns of every q-tile
-        uint32_t z[16];
-#pragma unroll
-        for (int k = 0; k < 16; ++k) z[k] = 0u;
-        for (int it = (CH ? u.it0 : 0); it < (CH ? u.it1 : p.nQT); ++it) ptx::tmem_st16(tmem + lane_off + kStripCol + (it - (CH ? u.it0 : 0)) * 64 + col, z);
-      }
       if (p.has_bias2) ptx::mbar_wait(bias_full, bph);
       for (int a = 0; a < cnt; ++a) {
         for (int it = (CH ? u.it0 : 0); it < (CH ? u.it1 : p.nQT); ++it) {
@@ -468,18 +489,13 @@ __global__ void __launch_bounds__(kThreads, 1)
           if (tid_wg == 0 && wg == 0) trace(p, kTbSSeen, step);
           ptx::mbar_wait(&pds_free[sb], ph ^ 1);  // P/dS buffer sb: MMAs of step-2 done
           ptx::tc_fence_after();
-          // all loads of the step in flight together: S, dP, the strip (TMEM) and the bias2 row (smem)
-          const uint32_t sa = tmem + lane_off + kStripCol + (it - (CH ? u.it0 : 0)) * 64 + col;
-          uint32_t sv[16], dp[16], acc[16];
+          // all loads of the step in flight together: S, dP (TMEM) and the bias2 row (smem)
+          uint32_t sv[16], dp[16];
           ptx::tmem_ld16(tmem + lane_off + sb * 128 + col, sv);
           ptx::tmem_ld16(tmem + lane_off + sb * 128 + 64 + col, dp);
-          if (p.dbias2) {
-            ptx::tmem_st_wait();
-            ptx::tmem_ld16(sa, acc);
-          }
           uint4 braw[2] = {make_uint4(0u, 0u, 0u, 0u), make_uint4(0u, 0u, 0u, 0u)};
           const uint32_t bt = ptx::smem_u32(sBias + (size_t)(it - (CH ? u.it0 : 0)) * C::kBiasTile) + r * 128;
-          if (p.has_bias2) {
+          if (p.has_bias2 && !(EVO_BWD_EXP & 4)) {
             braw[0] = lds128(bt + ((uint32_t)((2 * wg) << 4) ^ r7));
             braw[1] = lds128(bt + ((uint32_t)((2 * wg + 1) << 4) ^ r7));
           }
@@ -500,9 +516,6 @@ __global__ void __launch_bounds__(kThreads, 1)
               pr.y = ex2(x.y);
               const float2 d =
                   __fmul2_rn(pr, __fadd2_rn(make_float2(__uint_as_float(dp[k]), __uint_as_float(dp[k + 1])), nd));
-              const float2 ac = __fadd2_rn(make_float2(__uint_as_float(acc[k]), __uint_as_float(acc[k + 1])), d);
-              acc[k] = __float_as_uint(ac.x);
-              acc[k + 1] = __float_as_uint(ac.y);
               pk[k / 2] = F16 ? ptx::pack_f16(pr.x, pr.y) : ptx::pack_bf16(pr.x, pr.y);
               dk[k / 2] = F16 ? ptx::pack_f16(d.x, d.y) : ptx::pack_bf16(d.x, d.y);
             }
@@ -511,7 +524,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           const uint32_t pbase = ptx::smem_u32(sP + sb * C::kPdsTile) + r * 128;
           const uint32_t dbase = ptx::smem_u32(sdS + sb * C::kPdsTile) + r * 128;
 #pragma unroll
-          for (int c = 0; c < 2; ++c) {
+          for (int c = 0; c < ((EVO_BWD_EXP & 8) ? 0 : 2); ++c) {
             const uint32_t off = (uint32_t)((2 * wg + c) << 4) ^ r7;
             sts128(pbase + off, make_uint4(pk[4 * c], pk[4 * c + 1], pk[4 * c + 2], pk[4 * c + 3]));
             sts128(dbase + off, make_uint4(dk[4 * c], dk[4 * c + 1], dk[4 * c + 2], dk[4 * c + 3]));
@@ -519,14 +532,16 @@ __global__ void __launch_bounds__(kThreads, 1)
           ptx::fence_proxy_async_smem();
           ptx::mbar_arrive(&pds_full[sb]);
           if (tid_wg == 0) trace(p, wg == 0 ? kTbPds0 : kTbPds1, step);
-          if (p.dbias2) ptx::tmem_st16(sa, acc);  // dBias2 strip += dS (fp32, TMEM)
           ++step;
           if (++qs == C::kQStages) { qs = 0; qph ^= 1; }
         }
       }
-      // ---- unit end: flush the dBias2 strip (fp32 red.add; one partial per CTA and unit)
+      // ---- unit end: flush the dBias2 strip (fp32 red.add; one partial per CTA and unit) once the
+      // unit's last strip MMA completed; the next unit's first strip MMA waits on this WG's next P/dS
       if (p.dbias2) {
-        ptx::tmem_st_wait();
+        ptx::mbar_wait(strip_full, uph);
+        uph ^= 1;
+        ptx::tc_fence_after();
         const int j0 = u.jt * kBN + (int)col;
         for (int it = (CH ? u.it0 : 0); it < (CH ? u.it1 : p.nQT); ++it) {
           const int i = it * kBM + r;
@@ -548,6 +563,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
         }
       }
+      if (p.dbias2) ptx::tc_fence_before();  // strip reads ordered before the next P/dS arrival (its MMAs overwrite)
       if (p.dbias2 && p.dbias2_mc) __threadfence_system();  // remote adds ordered before the ranks' barrier
       if (p.has_bias2) {
         ptx::named_bar_sync(1 + wg, 128);

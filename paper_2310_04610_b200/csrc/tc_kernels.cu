@@ -215,9 +215,9 @@ size_t bwd_smem_bytes(int nQT) {
   size_t b = 1024;
   b += (size_t)C::kQStages * 2 * C::kTileQ + (size_t)C::kKStages * 2 * C::kTileK + 4 * (size_t)C::kPdsTile;
   b += (size_t)nQT * C::kBiasTile + 2 * (size_t)bk::kBM * D * 4;
-  b += (size_t)bk::kAugA + (size_t)C::kKStages * bk::kAugB + bk::kOnes;
+  b += (size_t)bk::kAugA + (size_t)C::kKStages * bk::kAugB + bk::kOnes + bk::kIdent;
   b += (size_t)C::kQStages * bk::kBM * 4 * 2 + (size_t)C::kKStages * 64 * 2;
-  b += (size_t)(2 * C::kQStages + 2 * C::kKStages + 8 + 6) * 8 + 16;
+  b += (size_t)(2 * C::kQStages + 2 * C::kKStages + 8 + 7) * 8 + 16;
   return b;
 }
 
