@@ -47,8 +47,8 @@ typedef enum {
 typedef enum { EVO_F32 = 0, EVO_BF16 = 1, EVO_F16 = 2 } evo_dtype;
 
 /* Kernel family selection. AUTO picks tcgen05 (sm_100a tensor cores) for
- * bf16/f16 with D in {16, 32, 64} (forward) and D in {16, 32}, L % 8 == 0,
- * no dbias1 (backward), and the SIMT (FFMA) kernels otherwise
+ * bf16/f16 with D in {16, 32, 64} (forward) and D in {16, 32}, L % 8 == 0
+ * (backward), and the SIMT (FFMA) kernels otherwise
  * (fp32 must not use TF32: it fails the 1e-4 parity bar). */
 typedef enum { EVO_PATH_AUTO = 0, EVO_PATH_SIMT = 1, EVO_PATH_TCGEN05 = 2 } evo_path;
 
@@ -71,6 +71,10 @@ typedef struct {
                              rank's replica receives the sum of all ranks: the cross-GPU reduction
                              happens inside the kernel. The caller zeroes all replicas and
                              synchronises the ranks before and after the call. NULL = local only. */
+  int need_dbias1;        /* backward: the call will ask for dbias1. Sizes the workspace for it (the
+                             tcgen05 backward then splits the query axis into chunks of 2 tiles and
+                             reduces dK/dV in fp32); a dbias1 request with need_dbias1 == 0 is a
+                             ValidationError. The reference has no bias1: 0 there. */
 } evo_attn_desc;
 
 size_t evo_attn_fwd_workspace_size(const evo_attn_desc* desc);

@@ -78,7 +78,7 @@ BwdWs bwd_layout(const evo_attn_desc* d) {
   w.db2 = off;
   if (d->has_bias2) off += align_up((size_t)d->Bo * d->H * d->L * d->L * 4);
   w.db1 = off;
-  if (d->has_bias1) off += align_up(B * d->L * 4);
+  if (d->has_bias1 && d->need_dbias1) off += align_up(B * d->L * 4);
   w.tc = off;
   off += align_up(evo::tc::bwd_scratch_bytes(d));
   w.total = off;
@@ -218,6 +218,8 @@ evo_status evo_attn_bwd(const evo_attn_desc* d, const void* dout, const void* q,
   if (d->has_bias1 != (bias1 != nullptr)) return fail(EVO_ERR_VALIDATION, "bias1 presence does not match the descriptor");
   if (d->has_bias2 != (bias2 != nullptr)) return fail(EVO_ERR_VALIDATION, "bias2 presence does not match the descriptor");
   if (dbias1 && !d->has_bias1) return fail(EVO_ERR_VALIDATION, "dbias1 requested without bias1");
+  if (dbias1 && !d->need_dbias1)
+    return fail(EVO_ERR_VALIDATION, "dbias1 requested but desc.need_dbias1 == 0 (workspace sized without it)");
   if (dbias2 && !d->has_bias2) return fail(EVO_ERR_VALIDATION, "dbias2 requested without bias2");
   if (accumulate_dbias && d->dbias_dtype != EVO_F32)
     return fail(EVO_ERR_VALIDATION, "accumulate_dbias requires dbias_dtype == EVO_F32");

@@ -22,6 +22,8 @@
 //    accumulator with TMA bulk reduce-add (one partial per 64-key tile), converted afterwards.
 //  TMEM: S/dP buffers [0,256), dBias strip [256, 256+64*nQT), dQ at 448, dK|dV at 480 (nQT <= 3).
 #pragma once
+#include <type_traits>
+
 #include "common.cuh"
 #include "tc_ptx.cuh"
 
@@ -44,6 +46,9 @@ constexpr int kOnes = 16 * 32;                           // 16 x 16 bf16 ones: t
 constexpr int kIdent = 16 * 32;                          // 16 x 16 identity: dBias2 strip += dS I on the tensor pipe
 constexpr uint32_t kStripCol = 256, kDqCol = 448, kDkvCol = 480;
 constexpr uint32_t kDb1Col = 384;
+#ifndef EVO_BWD_QS
+#define EVO_BWD_QS 4
+#endif
 #ifndef EVO_BWD_EXP
 #define EVO_BWD_EXP 0  // timing experiments only (wrong results), bit mask: 1 no dK/dV MMAs, 2 no dQ MMA, 4 no bias LDS, 8 no P/dS stores
 #endif  // dBias1 column sums (M=64, 16 columns) when requested: chunks of <= 2 q-tiles
@@ -53,7 +58,9 @@ struct Cfg {
   static constexpr int kRowBytes = D * 2;
   static constexpr int kTileQ = kBM * kRowBytes;    // Q or dO tile
   static constexpr int kTileK = kBN * kRowBytes;    // K or V tile
-  static constexpr int kQStages = 3;                // (Q, dO, lse, delta) ring
+  static constexpr int kQStages = EVO_BWD_QS;       // (Q, dO, lse, delta) ring: a slot refills only once the
+                                                    // gradient MMAs of its step completed, so depth = TMA slack
+  static constexpr int kDqBufs = kQStages > 3 ? 1 : 2;  // fp32 dQ staging tiles (shared-memory budget)
   static constexpr int kKStages = 2;                // (K, V, bias1 chunk) ring
   static constexpr int kBiasTile = kBM * kBN * 2;   // 16 KB
   static constexpr int kPdsTile = kBM * kBN * 2;    // 16 KB (P or dS, bf16)
@@ -174,8 +181,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint8_t* sP = sV + C::kKStages * C::kTileK;                  // [2] P tiles (bf16, SW128)
   uint8_t* sdS = sP + 2 * C::kPdsTile;                         // [2] dS tiles
   uint8_t* sBias = sdS + 2 * C::kPdsTile;                      // [nQT] bias strip tiles
-  float* sDq = (float*)(sBias + (size_t)p.nQC * C::kBiasTile);  // [2] dQ staging (fp32 128 x D)
-  uint8_t* sAaug = (uint8_t*)(sDq + 2 * kBM * D);              // 128 x 16 (1/scale split), SW32
+  float* sDq = (float*)(sBias + (size_t)p.nQC * C::kBiasTile);  // dQ staging (fp32 128 x D)
+  uint8_t* sAaug = (uint8_t*)(sDq + C::kDqBufs * kBM * D);     // 128 x 16 (1/scale split), SW32
   uint8_t* sBaug = sAaug + kAugA;                              // [KS] 64 x 16 (bias1 per key), SW32
   uint8_t* sOnes = sBaug + C::kKStages * kAugB;                // 16 x 16 ones (dBias1 = dS^T 1), SW32
   uint8_t* sIdent = sOnes + kOnes;                             // 16 x 16 identity (strip += dS I), SW32
@@ -346,6 +353,13 @@ __global__ void __launch_bounds__(kThreads, 1)
           const uint32_t doB = do0n + qs * (C::kTileQ >> 4);
           const uint32_t kB = k0n + ks * (C::kTileK >> 4);
           if (ptx::elect_one()) {
+            trace(p, kTbGradsStart, step);
+            // dQ first: the epilogue drains it while dK / dV run, so the next step's dQ never waits
+#pragma unroll
+            for (int kk = 0; kk < ((EVO_BWD_EXP & 2) ? 0 : kBN / 16); ++kk)  // dQ = dS K: K = 64 keys (+32 B in the dS rows)
+              ptx::mma_ss(tdQ, ptx::desc_make(dsK + kk * 2, kHiP), ptx::desc_make(kB + kk * kRow16, kHiMN), idQ,
+                          kk > 0);
+            ptx::tc_commit(dq_full);
 #pragma unroll
             for (int kk = 0; kk < ((EVO_BWD_EXP & 1) ? 0 : kBM / 16); ++kk) {  // K = 128 queries: 16 rows per step
               // A = P^T / dS^T: MN-major SW128 (64 keys wide), 16 query rows = 2 x 8-row atoms (+2048 B)
@@ -358,11 +372,6 @@ __global__ void __launch_bounds__(kThreads, 1)
               if (p.dbias1)  // dBias1 partial: dS^T (keys x queries) times a ones column block
                 ptx::mma_ss(tmem + kDb1Col, ptx::desc_make(dsA + kk * 128, kHiP), bOnes, idB1, acc);
             }
-#pragma unroll
-            for (int kk = 0; kk < ((EVO_BWD_EXP & 2) ? 0 : kBN / 16); ++kk)  // dQ = dS K: K = 64 keys (+32 B in the dS rows)
-              ptx::mma_ss(tdQ, ptx::desc_make(dsK + kk * 2, kHiP), ptx::desc_make(kB + kk * kRow16, kHiMN), idQ,
-                          kk > 0);
-            ptx::tc_commit(dq_full);
             if (p.dbias2) {
               // dBias2 strip (this q-tile's 128 x 64 fp32 block in TMEM) += dS: four N = 16 column blocks,
               // dS block kk (K-major, 16 keys) times a 16 x 16 identity; the unit's first row initialises
@@ -531,7 +540,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
           ptx::fence_proxy_async_smem();
           ptx::mbar_arrive(&pds_full[sb]);
-          if (tid_wg == 0) trace(p, wg == 0 ? kTbPds0 : kTbPds1, step);
+          if (tid_wg == 0 && (wg == 0 || wg == kSoftWG - 1)) trace(p, wg == 0 ? kTbPds0 : kTbPds1, step);
           ++step;
           if (++qs == C::kQStages) { qs = 0; qph ^= 1; }
         }
@@ -596,8 +605,10 @@ __global__ void __launch_bounds__(kThreads, 1)
           ptx::tmem_ld_wait();
           ptx::tc_fence_before();
           ptx::mbar_arrive(dq_free);
-          float* stg = sDq + (step & 1) * kBM * D;
-          if (tid_e == 0) ptx::bulk_wait_read<1>();  // staging buffer of step-2 has been read by TMA
+          float* stg = sDq + (C::kDqBufs == 2 ? (step & 1) * kBM * D : 0);
+          if (tid_e == 0) {  // the reduce that last used this staging tile has read it
+            if constexpr (C::kDqBufs == 2) ptx::bulk_wait_read<1>(); else ptx::bulk_wait_read<0>();
+          }
           ptx::named_bar_sync(kEpiBar, 128);
           // row r of the staging tile, 16B chunks swizzled like the fp32 dQ tensor map (D*4-byte rows)
           const uint32_t sa = ptx::smem_u32(stg) + r * (D * 4);
@@ -636,8 +647,10 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (CH && p.dkv_reduce) {
           // this query chunk's dK / dV partial of the row: fp32 rows (dK 0-63, dV 64-127) into a staging
           // tile, TMA reduce-add into the fp32 accumulators (scaled and converted after the kernel)
-          float* stg = sDq + (step & 1) * kBM * D;
-          if (tid_e == 0) ptx::bulk_wait_read<1>();  // the previous user of this buffer was read
+          float* stg = sDq + (C::kDqBufs == 2 ? (step & 1) * kBM * D : 0);
+          if (tid_e == 0) {  // the previous user of this staging tile was read
+            if constexpr (C::kDqBufs == 2) ptx::bulk_wait_read<1>(); else ptx::bulk_wait_read<0>();
+          }
           ptx::named_bar_sync(kEpiBar, 128);
           const uint32_t sa = ptx::smem_u32(stg) + (krow + (isk ? 0 : 64)) * (D * 4);
 #pragma unroll
@@ -681,7 +694,8 @@ __global__ void __launch_bounds__(kThreads, 1)
 
 // Backward preamble (one pass over dO and O): delta[b,h,i] = sum_d dO*O (attention_tiled.cpp:254-262)
 // and lse2 = lse * log2e, both laid out [B, H, Lp] with the rows past L padded (+inf / 0).
-// Thread per (b, i, h): D contiguous elements of dO and O, 16-byte loads.
+// Thread per (b, i, h): D contiguous elements of dO and O, 16-byte loads (neighbouring threads read
+// neighbouring rows: the dO / O streams, 2/3 of the bytes, are fully contiguous).
 template <int D, typename T>
 __global__ void prep_kernel(const T* __restrict__ dout, const T* __restrict__ o, const float* __restrict__ lse,
                             float* __restrict__ lse2, float* __restrict__ delta_p, int B, int L, int H, int Lp,
@@ -734,17 +748,26 @@ __global__ void pad_rows_kernel(const float* __restrict__ lse, const float* __re
   }
 }
 
-// dQ (bf16/f16) = scale * dQacc (fp32)
+// dQ (bf16/f16) = scale * dQacc (fp32); 8 elements per thread and iteration (n % 8 == 0: D >= 16):
+// two 16-byte loads, one 16-byte store
 template <typename T>
 __global__ void dq_convert_kernel(const float* __restrict__ acc, T* __restrict__ dq, size_t n, float scale) {
   ptx::pdl_wait();  // programmatic dependent of the main kernel
   ptx::pdl_launch_dependents();
-  for (size_t x = (blockIdx.x * (size_t)blockDim.x + threadIdx.x) * 4; x < n; x += (size_t)gridDim.x * blockDim.x * 4) {
-    const float4 v = *(const float4*)(acc + x);
-    dq[x] = from_f<T>(v.x * scale);
-    dq[x + 1] = from_f<T>(v.y * scale);
-    dq[x + 2] = from_f<T>(v.z * scale);
-    dq[x + 3] = from_f<T>(v.w * scale);
+  constexpr bool F16 = std::is_same<T, __half>::value;
+  if (((uintptr_t)dq & 15) != 0) {  // caller buffer not 16-byte aligned: element stores
+    for (size_t x = blockIdx.x * (size_t)blockDim.x + threadIdx.x; x < n; x += (size_t)gridDim.x * blockDim.x)
+      dq[x] = from_f<T>(acc[x] * scale);
+    return;
+  }
+  for (size_t x = (blockIdx.x * (size_t)blockDim.x + threadIdx.x) * 8; x < n; x += (size_t)gridDim.x * blockDim.x * 8) {
+    const float4 a = __ldcs((const float4*)(acc + x)), c = __ldcs((const float4*)(acc + x + 4));
+    uint4 w;
+    w.x = F16 ? ptx::pack_f16(a.x * scale, a.y * scale) : ptx::pack_bf16(a.x * scale, a.y * scale);
+    w.y = F16 ? ptx::pack_f16(a.z * scale, a.w * scale) : ptx::pack_bf16(a.z * scale, a.w * scale);
+    w.z = F16 ? ptx::pack_f16(c.x * scale, c.y * scale) : ptx::pack_bf16(c.x * scale, c.y * scale);
+    w.w = F16 ? ptx::pack_f16(c.z * scale, c.w * scale) : ptx::pack_bf16(c.z * scale, c.w * scale);
+    *(uint4*)(dq + x) = w;
   }
 }
 

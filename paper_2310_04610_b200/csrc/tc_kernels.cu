@@ -200,8 +200,8 @@ BwdScratch bwd_scratch_layout(const evo_attn_desc* d) {
   const size_t acc = align256(B * d->L * d->H * d->D * 4);
   w.dq = 0;
   w.dk = acc;
-  // dK/dV accumulators when the query axis may be chunked (a dBias1 request chunks by 2 tiles)
-  const bool may_chunk = bwd_nic(d, d->has_bias1 != 0) > 1;
+  // dK/dV accumulators when the query axis is chunked (a dBias1 request chunks by 2 tiles)
+  const bool may_chunk = bwd_nic(d, d->has_bias1 && d->need_dbias1) > 1;
   w.dv = w.dk + (may_chunk ? acc : 0);
   w.lse2 = w.dv + (may_chunk ? acc : 0);
   w.delta = w.lse2 + align256(B * d->H * Lp * 4);
@@ -214,7 +214,7 @@ size_t bwd_smem_bytes(int nQT) {
   using C = bk::Cfg<D>;
   size_t b = 1024;
   b += (size_t)C::kQStages * 2 * C::kTileQ + (size_t)C::kKStages * 2 * C::kTileK + 4 * (size_t)C::kPdsTile;
-  b += (size_t)nQT * C::kBiasTile + 2 * (size_t)bk::kBM * D * 4;
+  b += (size_t)nQT * C::kBiasTile + (size_t)C::kDqBufs * bk::kBM * D * 4;
   b += (size_t)bk::kAugA + (size_t)C::kKStages * bk::kAugB + bk::kOnes + bk::kIdent;
   b += (size_t)C::kQStages * bk::kBM * 4 * 2 + (size_t)C::kKStages * 64 * 2;
   b += (size_t)(2 * C::kQStages + 2 * C::kKStages + 8 + 7) * 8 + 16;
@@ -323,7 +323,7 @@ evo_status launch_bwd(const evo_attn_desc* d, const Shape& s, const void* dout, 
   }
   ++*launches;
   const size_t n = (size_t)s.B * s.L * s.H * D;
-  const unsigned cg = (unsigned)std::min<size_t>((n / 4 + 255) / 256, 148 * 32);
+  const unsigned cg = (unsigned)std::min<size_t>((n / 8 + 255) / 256, 148 * 16);
   auto convert = [&](const float* acc, void* out, float scale) {  // programmatic dependents of the main kernel
     cudaLaunchConfig_t cfg = {};
     cudaLaunchAttribute attr[1];

@@ -110,6 +110,7 @@ def evoformer_attention_backward(dout, q, k, v, o, lse, bias1=None, bias2=None, 
             db1 = torch.empty(bias1.shape, device=q.device, dtype=odt)
         if need_dbias2 and bias2 is not None:
             db2 = torch.empty(bias2.shape, device=q.device, dtype=odt)
+    d.need_dbias1 = int(db1 is not None)  # sizes the workspace for the dBias1 path only when asked
     wsb = lib.evo_attn_bwd_workspace_size(d)
     ws = torch.empty(max(wsb, 1), device=q.device, dtype=torch.uint8)
     N.check(lib.evo_attn_bwd(d, _ptr(dout.contiguous()), _ptr(q), _ptr(k), _ptr(v), _ptr(bias1),

@@ -45,11 +45,17 @@ def test_workspace_sizes():
     from paper_2310_04610_b200 import _native as N
 
     lib = N.load()
-    d = _desc()
+    d = _desc(need_dbias1=1)
     ws = lib.evo_attn_bwd_workspace_size(d)
     # delta (B*H*L f32) + dbias2 fp32 (H*L*L) + dbias1 (B*L) at least
     assert ws >= 4 * (4 * 2 * 64 + 2 * 64 * 64 + 4 * 64)
     assert lib.evo_attn_bwd_workspace_size(_desc(L=0)) == 0
+    # the dBias1 path (query chunks of 2 tiles, fp32 dK/dV) is only budgeted when asked for: at
+    # L = 384 it adds two fp32 [B, L, H, D] accumulators
+    acc = 4 * 4 * 384 * 2 * 32
+    plain = lib.evo_attn_bwd_workspace_size(_desc(L=384))
+    with_db1 = lib.evo_attn_bwd_workspace_size(_desc(L=384, need_dbias1=1))
+    assert with_db1 - plain >= 2 * acc
 
 
 def test_status_codes_without_gpu():

@@ -27,7 +27,7 @@ torch.cuda.synchronize()
 lib.evo_attn_debug_set_trace_bwd(None)
 t = buf.view(12, 64).cpu().tolist()
 t0 = min(x for row in t for x in row if x > 0)
-names = ["S_issue", "S_seen", "Pds_wg0", "Pds_wg1", "Grads", "Dq_seen", "Dq_out", "Q_full", "ProdQ", "K_full", "GradsSt", "S_done"]
+names = ["S_issue", "S_seen", "Pds_wg0", "Pds_wg3", "Grads", "Dq_seen", "Dq_out", "Q_full", "ProdQ", "K_full", "GradsSt", "S_done"]
 if "--phase" in sys.argv:  # library built with -DEVO_BWD_PHASE_TRACE=1
     names[7:12] = ["ph_qfull", "ph_ldtm", "ph_math", "ph_sts", "ph_waits"]
 print("step " + " ".join(f"{n:>9s}" for n in names))
