@@ -20,7 +20,7 @@ torch.cuda.synchronize()
 lib.evo_attn_debug_set_trace(None)
 t = buf.view(12, 64).cpu().tolist()
 t0 = min(x for row in t for x in row if x > 0)
-names = ["Vload", "S_issue", "S_seen", "P_wg0", "P_wg1", "PV_issue", "RowEnd", "RowStart", "Pfull_ok", "Vfull_ok", "-", "-"]
+names = ["Vload", "S_issue", "S_seen", "P_wg0", "P_wg1", "PV_issue", "RowEnd", "RowStart", "Pfull_ok", "Vfull_ok", "Kload", "Kfull_ok"]
 print("tile " + " ".join(f"{n:>9s}" for n in names))
 for tile in range(40):
     print(f"{tile:4d} " + " ".join(f"{(t[e][tile] - t0) if t[e][tile] else -1:9d}" for e in range(12)))
