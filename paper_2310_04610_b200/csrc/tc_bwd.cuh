@@ -31,11 +31,19 @@ namespace evo {
 namespace tc {
 namespace bk {
 
+#ifndef EVO_BWD_ALT
+#define EVO_BWD_ALT 1  // softmax warpgroups take turns on the steps: 0 all 4 on every step, 1 two groups of 2, 2 one at a time
+#endif
 constexpr int kBM = 128;   // queries per tile
 constexpr int kBN = 64;    // keys per tile
 // warps: 0 TMA producer, 1 gradient MMAs, 2 S/dP MMAs, 3..3+4*kSoftWG softmax warpgroups, then the epilogue WG
 constexpr int kSoftWG = 4;                              // softmax warpgroups, 16 keys each
 constexpr int kKeysPerThread = 64 / kSoftWG;
+// kGroups groups of softmax warpgroups take turns on the steps (step % kGroups): a group's warpgroup
+// covers kGroups 16-key blocks of its step, so one group's TMEM / shared-memory phases overlap the
+// other's exponentials instead of all warpgroups running the same phase at once
+constexpr int kGroups = EVO_BWD_ALT == 2 ? 4 : EVO_BWD_ALT ? 2 : 1;
+constexpr int kGroupThreads = 128 * kSoftWG / kGroups;
 constexpr int kSoftWarp0 = 3;
 constexpr int kEpiWarp0 = kSoftWarp0 + 4 * kSoftWG;
 constexpr int kThreads = (kEpiWarp0 + 4) * 32;
@@ -217,8 +225,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     for (int s = 0; s < C::kKStages; ++s) { ptx::mbar_init(&k_full[s], 1); ptx::mbar_init(&k_empty[s], 1); }
     for (int s = 0; s < 2; ++s) {
       ptx::mbar_init(&s_full[s], 1);
-      ptx::mbar_init(&s_free[s], kSoftThreads);
-      ptx::mbar_init(&pds_full[s], kSoftThreads);
+      ptx::mbar_init(&s_free[s], kGroupThreads);   // buffer s serves the group of steps s (mod 2)
+      ptx::mbar_init(&pds_full[s], kGroupThreads);
       ptx::mbar_init(&pds_free[s], 1);
     }
     ptx::mbar_init(dq_full, 1);
@@ -476,7 +484,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int r = q4 * 32 + lane;                 // query row in tile == TMEM lane
     const int tid_wg = (warp - kSoftWarp0 - 4 * wg) * 32 + lane;
     const uint32_t lane_off = (uint32_t)(q4 * 32) << 16;
-    const uint32_t col = (uint32_t)(wg * kKeysPerThread);
+    const uint32_t col = (uint32_t)(wg * kKeysPerThread);  // this warpgroup's strip columns (flush)
+    const int grp = wg / (kSoftWG / kGroups), sub = wg % (kSoftWG / kGroups);
     const float2 scl2 = make_float2(p.scale_log2, p.scale_log2);
     const float2 lg2 = make_float2(kLog2e, kLog2e);
     const uint32_t r7 = (uint32_t)(r & 7) << 4;
@@ -489,6 +498,11 @@ __global__ void __launch_bounds__(kThreads, 1)
       for (int a = 0; a < cnt; ++a) {
         for (int it = (CH ? u.it0 : 0); it < (CH ? u.it1 : p.nQT); ++it) {
           const uint32_t sb = step & 1, ph = (step >> 1) & 1;
+          if ((int)(step % kGroups) != grp) {  // the other group's step
+            ++step;
+            if (++qs == C::kQStages) { qs = 0; qph ^= 1; }
+            continue;
+          }
           ptx::mbar_wait(&q_full[qs], qph);
           const float lse2 = ptx::lds_f32(ptx::smem_u32(sLse + qs * kBM + r));
           const float dl = ptx::lds_f32(ptx::smem_u32(sDel + qs * kBM + r));
@@ -498,45 +512,52 @@ __global__ void __launch_bounds__(kThreads, 1)
           if (tid_wg == 0 && wg == 0) trace(p, kTbSSeen, step);
           ptx::mbar_wait(&pds_free[sb], ph ^ 1);  // P/dS buffer sb: MMAs of step-2 done
           ptx::tc_fence_after();
-          // all loads of the step in flight together: S, dP (TMEM) and the bias2 row (smem)
-          uint32_t sv[16], dp[16];
-          ptx::tmem_ld16(tmem + lane_off + sb * 128 + col, sv);
-          ptx::tmem_ld16(tmem + lane_off + sb * 128 + 64 + col, dp);
-          uint4 braw[2] = {make_uint4(0u, 0u, 0u, 0u), make_uint4(0u, 0u, 0u, 0u)};
           const uint32_t bt = ptx::smem_u32(sBias + (size_t)(it - (CH ? u.it0 : 0)) * C::kBiasTile) + r * 128;
-          if (p.has_bias2 && !(EVO_BWD_EXP & 4)) {
-            braw[0] = lds128(bt + ((uint32_t)((2 * wg) << 4) ^ r7));
-            braw[1] = lds128(bt + ((uint32_t)((2 * wg + 1) << 4) ^ r7));
-          }
-          ptx::tmem_ld_wait();
-          ptx::tc_fence_before();
-          ptx::mbar_arrive(&s_free[sb]);  // S/dP buffer may be recomputed
-          uint32_t pk[8], dk[8];
-#pragma unroll
-          for (int c = 0; c < 2; ++c) {
-            const uint32_t wv[4] = {braw[c].x, braw[c].y, braw[c].z, braw[c].w};
-#pragma unroll
-            for (int e = 0; e < 4; ++e) {
-              const int k = c * 8 + 2 * e;
-              const float2 bb = __ffma2_rn(unpack2<F16>(wv[e]), lg2, nl);  // bias2 * log2e - lse * log2e
-              const float2 x = __ffma2_rn(make_float2(__uint_as_float(sv[k]), __uint_as_float(sv[k + 1])), scl2, bb);
-              float2 pr;
-              pr.x = ex2(x.x);
-              pr.y = ex2(x.y);
-              const float2 d =
-                  __fmul2_rn(pr, __fadd2_rn(make_float2(__uint_as_float(dp[k]), __uint_as_float(dp[k + 1])), nd));
-              pk[k / 2] = F16 ? ptx::pack_f16(pr.x, pr.y) : ptx::pack_bf16(pr.x, pr.y);
-              dk[k / 2] = F16 ? ptx::pack_f16(d.x, d.y) : ptx::pack_bf16(d.x, d.y);
-            }
-          }
-          // P and dS -> shared (128B swizzle; chunks 2wg, 2wg+1 of row r)
           const uint32_t pbase = ptx::smem_u32(sP + sb * C::kPdsTile) + r * 128;
           const uint32_t dbase = ptx::smem_u32(sdS + sb * C::kPdsTile) + r * 128;
+#pragma unroll 1
+          for (int cb = 0; cb < kGroups; ++cb) {
+            const int kb = sub * kGroups + cb;  // 16-key block of the step
+            const uint32_t col = (uint32_t)(kb * 16);
+            // all loads of the block in flight together: S, dP (TMEM) and the bias2 row (smem)
+            uint32_t sv[16], dp[16];
+            ptx::tmem_ld16(tmem + lane_off + sb * 128 + col, sv);
+            ptx::tmem_ld16(tmem + lane_off + sb * 128 + 64 + col, dp);
+            uint4 braw[2] = {make_uint4(0u, 0u, 0u, 0u), make_uint4(0u, 0u, 0u, 0u)};
+            if (p.has_bias2 && !(EVO_BWD_EXP & 4)) {
+              braw[0] = lds128(bt + ((uint32_t)((2 * kb) << 4) ^ r7));
+              braw[1] = lds128(bt + ((uint32_t)((2 * kb + 1) << 4) ^ r7));
+            }
+            ptx::tmem_ld_wait();
+            if (cb == kGroups - 1) {
+              ptx::tc_fence_before();
+              ptx::mbar_arrive(&s_free[sb]);  // S/dP buffer may be recomputed
+            }
+            uint32_t pk[8], dk[8];
 #pragma unroll
-          for (int c = 0; c < ((EVO_BWD_EXP & 8) ? 0 : 2); ++c) {
-            const uint32_t off = (uint32_t)((2 * wg + c) << 4) ^ r7;
-            sts128(pbase + off, make_uint4(pk[4 * c], pk[4 * c + 1], pk[4 * c + 2], pk[4 * c + 3]));
-            sts128(dbase + off, make_uint4(dk[4 * c], dk[4 * c + 1], dk[4 * c + 2], dk[4 * c + 3]));
+            for (int c = 0; c < 2; ++c) {
+              const uint32_t wv[4] = {braw[c].x, braw[c].y, braw[c].z, braw[c].w};
+#pragma unroll
+              for (int e = 0; e < 4; ++e) {
+                const int k = c * 8 + 2 * e;
+                const float2 bb = __ffma2_rn(unpack2<F16>(wv[e]), lg2, nl);  // bias2 * log2e - lse * log2e
+                const float2 x = __ffma2_rn(make_float2(__uint_as_float(sv[k]), __uint_as_float(sv[k + 1])), scl2, bb);
+                float2 pr;
+                pr.x = ex2(x.x);
+                pr.y = ex2(x.y);
+                const float2 d =
+                    __fmul2_rn(pr, __fadd2_rn(make_float2(__uint_as_float(dp[k]), __uint_as_float(dp[k + 1])), nd));
+                pk[k / 2] = F16 ? ptx::pack_f16(pr.x, pr.y) : ptx::pack_bf16(pr.x, pr.y);
+                dk[k / 2] = F16 ? ptx::pack_f16(d.x, d.y) : ptx::pack_bf16(d.x, d.y);
+              }
+            }
+            // P and dS -> shared (128B swizzle; chunks 2kb, 2kb+1 of row r)
+#pragma unroll
+            for (int c = 0; c < ((EVO_BWD_EXP & 8) ? 0 : 2); ++c) {
+              const uint32_t off = (uint32_t)((2 * kb + c) << 4) ^ r7;
+              sts128(pbase + off, make_uint4(pk[4 * c], pk[4 * c + 1], pk[4 * c + 2], pk[4 * c + 3]));
+              sts128(dbase + off, make_uint4(dk[4 * c], dk[4 * c + 1], dk[4 * c + 2], dk[4 * c + 3]));
+            }
           }
           ptx::fence_proxy_async_smem();
           ptx::mbar_arrive(&pds_full[sb]);
