@@ -57,6 +57,9 @@ constexpr uint32_t kDb1Col = 384;
 #ifndef EVO_BWD_QS
 #define EVO_BWD_QS 4
 #endif
+#ifndef EVO_BWD_POLY
+#define EVO_BWD_POLY 0
+#endif
 #ifndef EVO_BWD_EXP
 #define EVO_BWD_EXP 0  // timing experiments only (wrong results), bit mask: 1 no dK/dV MMAs, 2 no dQ MMA, 4 no bias LDS, 8 no P/dS stores
 #endif  // dBias1 column sums (M=64, 16 columns) when requested: chunks of <= 2 q-tiles
@@ -543,8 +546,12 @@ __global__ void __launch_bounds__(kThreads, 1)
                 const float2 bb = __ffma2_rn(unpack2<F16>(wv[e]), lg2, nl);  // bias2 * log2e - lse * log2e
                 const float2 x = __ffma2_rn(make_float2(__uint_as_float(sv[k]), __uint_as_float(sv[k + 1])), scl2, bb);
                 float2 pr;
-                pr.x = ex2(x.x);
-                pr.y = ex2(x.y);
+                if (EVO_BWD_POLY && e == 3) {
+                  pr = ex2_poly2(x);  // one pair in four on the FMA pipe (relieves MUFU)
+                } else {
+                  pr.x = ex2(x.x);
+                  pr.y = ex2(x.y);
+                }
                 const float2 d =
                     __fmul2_rn(pr, __fadd2_rn(make_float2(__uint_as_float(dp[k]), __uint_as_float(dp[k + 1])), nd));
                 pk[k / 2] = F16 ? ptx::pack_f16(pr.x, pr.y) : ptx::pack_bf16(pr.x, pr.y);

@@ -156,8 +156,21 @@ def test_tc_backward_many_rows_per_cta():
     check((1, 300, 128, 1, 32), "bf16")
 
 
-@pytest.mark.parametrize("shape", [(1, 4, 384, 2, 32), (2, 2, 200, 2, 32)])
-def test_tc_backward_dbias1(shape):
+@pytest.mark.parametrize("shape,dtype", [((1, 4, 384, 2, 32), "bf16"), ((2, 2, 200, 2, 32), "bf16"),
+                                         ((1, 2, 640, 2, 32), "bf16"), ((1, 3, 200, 2, 16), "f16")])
+def test_tc_backward_dbias1(shape, dtype):
     # the mask-bias gradient on the tcgen05 path: column sums of dS from an extra UMMA against a ones
-    # block (L = 384 runs in chunks of 2 query tiles to free the TMEM columns)
-    check(shape, "bf16", need_dbias1=True)
+    # block (L = 384 and 640 run in chunks of 2 query tiles to free the TMEM columns)
+    check(shape, dtype, need_dbias1=True)
+
+
+def test_tc_backward_dbias1_stays_on_tcgen05():
+    import paper_2310_04610_b200 as E
+
+    q, k, v, do, b1, b2 = make_inputs(1, 2, 384, 2, 32, seed=3)
+    t = lambda a: torch.tensor(a, dtype=torch.bfloat16, device="cuda")
+    o, lse = E.evoformer_attention_forward(t(q), t(k), t(v), t(b1), t(b2))
+    E.evoformer_attention_backward(t(do), t(q), t(k), t(v), o, lse, t(b1), t(b2), need_dbias1=True)
+    torch.cuda.synchronize()
+    # prep, main (2 query chunks), dQ / dK / dV conversions: the chunked tcgen05 path, not SIMT
+    assert E.last_launch_count() == 5
