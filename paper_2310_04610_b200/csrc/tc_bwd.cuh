@@ -82,6 +82,7 @@ struct Params {
   int B, N, L, H, Bo;
   int nQT, nKT;
   int nQC, nIC;      // query tiles per chunk (<= 3: the dBias2 strip of a chunk fits TMEM), chunks
+  int nBT;           // pair-bias tiles resident in shared memory (nQC, or 0 without bias2)
   long long total;   // items = Bo*H*nKT*nIC*N
   int aligned, split;
   float scale, scale_log2;
@@ -192,7 +193,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint8_t* sP = sV + C::kKStages * C::kTileK;                  // [2] P tiles (bf16, SW128)
   uint8_t* sdS = sP + 2 * C::kPdsTile;                         // [2] dS tiles
   uint8_t* sBias = sdS + 2 * C::kPdsTile;                      // [nQT] bias strip tiles
-  float* sDq = (float*)(sBias + (size_t)p.nQC * C::kBiasTile);  // dQ staging (fp32 128 x D)
+  float* sDq = (float*)(sBias + (size_t)p.nBT * C::kBiasTile);  // dQ staging (fp32 128 x D)
   uint8_t* sAaug = (uint8_t*)(sDq + C::kDqBufs * kBM * D);     // 128 x 16 (1/scale split), SW32
   uint8_t* sBaug = sAaug + kAugA;                              // [KS] 64 x 16 (bias1 per key), SW32
   uint8_t* sOnes = sBaug + C::kKStages * kAugB;                // 16 x 16 ones (dBias1 = dS^T 1), SW32

@@ -187,7 +187,11 @@ struct BwdScratch {
 constexpr int kBwdChunk = 3;  // query tiles per backward unit: its dBias2 strip (3 x 64 TMEM columns) fits
 int bwd_nqt(const evo_attn_desc* d) { return (int)((d->L + bk::kBM - 1) / bk::kBM); }
 // dBias1 needs 16 TMEM columns: its chunks hold 2 query tiles (strip 128 columns) instead of 3
-int bwd_chunk(const evo_attn_desc* d, bool db1) { return std::min(bwd_nqt(d), db1 ? 2 : kBwdChunk); }
+// without a pair bias there is no dBias2 strip in TMEM and no bias strip in shared memory: the whole
+// query axis is one chunk at any L (MSA column attention: bias-free plus mask, L = N_seq)
+int bwd_chunk(const evo_attn_desc* d, bool db1) {
+  return d->has_bias2 ? std::min(bwd_nqt(d), db1 ? 2 : kBwdChunk) : bwd_nqt(d);
+}
 int bwd_nic(const evo_attn_desc* d, bool db1 = false) {
   const int c = bwd_chunk(d, db1);
   return (bwd_nqt(d) + c - 1) / c;
@@ -277,7 +281,8 @@ evo_status launch_bwd(const evo_attn_desc* d, const Shape& s, const void* dout, 
   // 16-bit two-term split of 1/scale, B_aug rows the bias1 value of each key.
   p.aug = (s.bias1 != nullptr || s.L % bk::kBN != 0) ? 1 : 0;
   p.aug_c = aug_split(1.0 / (double)s.scale, F16);
-  const size_t smem = bwd_smem_bytes<D>(p.nQC);
+  p.nBT = s.bias2 ? p.nQC : 0;  // resident pair-bias tiles
+  const size_t smem = bwd_smem_bytes<D>(p.nBT);
   if (smem > kMaxSmem) {
     *err = "backward shared-memory budget exceeded";
     return EVO_ERR_UNSUPPORTED;

@@ -174,3 +174,19 @@ def test_tc_backward_dbias1_stays_on_tcgen05():
     torch.cuda.synchronize()
     # prep, main (2 query chunks), dQ / dK / dV conversions: the chunked tcgen05 path, not SIMT
     assert E.last_launch_count() == 5
+
+
+@pytest.mark.parametrize("shape,need_dbias1", [((1, 2, 1024, 2, 32), False), ((1, 2, 640, 2, 32), True),
+                                               ((2, 2, 520, 1, 16), False)])
+def test_tc_backward_msa_col_unchunked(shape, need_dbias1):
+    # MSA column attention (bias-free plus mask, the attended axis is N_seq): without a pair bias
+    # there is no dBias2 strip, so the tcgen05 backward takes the whole query axis in one chunk
+    check(shape, "bf16", bias2=False, need_dbias1=need_dbias1)
+    q, k, v, do, b1, _ = make_inputs(*shape, dtype="bf16", bias2=False, seed=5)
+    import paper_2310_04610_b200 as E
+
+    t = lambda a: torch.tensor(a, dtype=torch.bfloat16, device="cuda")
+    o, lse = E.evoformer_attention_forward(t(q), t(k), t(v), t(b1))
+    E.evoformer_attention_backward(t(do), t(q), t(k), t(v), o, lse, t(b1), None, need_dbias1=need_dbias1)
+    torch.cuda.synchronize()
+    assert E.last_launch_count() == 3  # prep, main, dQ conversion: no dK/dV chunk reduction
