@@ -226,7 +226,8 @@ def main():
     ap.add_argument("--config", default="c4", choices=sorted(CONFIGS))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--e2e-steps", type=int, default=5)
+    ap.add_argument("--e2e-steps", type=int, default=20,
+                    help="end-to-end steps timed (pipeline fill and drain amortised over them)")
     ap.add_argument("--all-configs", action="store_true", help="also time c1..c5 and attach them")
     ap.add_argument("--scaling", default="weak", choices=["weak", "strong"],
                     help="weak: each rank owns a full config's rows; strong: the config's rows split over ranks")
