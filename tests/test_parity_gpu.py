@@ -190,3 +190,28 @@ def test_tc_backward_msa_col_unchunked(shape, need_dbias1):
     E.evoformer_attention_backward(t(do), t(q), t(k), t(v), o, lse, t(b1), None, need_dbias1=need_dbias1)
     torch.cuda.synchronize()
     assert E.last_launch_count() == 3  # prep, main, dQ conversion: no dK/dV chunk reduction
+
+
+def test_dbias1_request_needs_descriptor_flag():
+    # the workspace is sized for the dBias1 path only when desc.need_dbias1 says so: a dbias1
+    # request without it is a ValidationError at the C-ABI, before any launch
+    import paper_2310_04610_b200 as E
+    from paper_2310_04610_b200 import _native as N
+    from paper_2310_04610_b200.evoformer_attention import make_desc
+
+    q, k, v, do, b1, b2 = make_inputs(1, 2, 384, 2, 32, seed=9)
+    t = lambda a: torch.tensor(a, dtype=torch.bfloat16, device="cuda")
+    tq, tk, tv, tdo, tb1, tb2 = map(t, (q, k, v, do, b1, b2))
+    o, lse = E.evoformer_attention_forward(tq, tk, tv, tb1, tb2)
+    d = make_desc(tq, tb1, tb2, None)
+    lib = N.load()
+    wsb = lib.evo_attn_bwd_workspace_size(d)
+    ws = torch.empty(wsb, device="cuda", dtype=torch.uint8)
+    g = [torch.empty_like(tq) for _ in range(3)]
+    db1 = torch.empty(tb1.shape, device="cuda", dtype=torch.float32)
+    db2 = torch.empty(tb2.shape, device="cuda", dtype=torch.float32)
+    p = lambda x: x.data_ptr()
+    st = lib.evo_attn_bwd(d, p(tdo), p(tq), p(tk), p(tv), p(tb1), p(tb2), p(o), p(lse), *map(p, g), p(db1),
+                          p(db2), 0, p(ws), wsb, torch.cuda.current_stream().cuda_stream)
+    assert st == N.EVO_ERR_VALIDATION
+    assert "need_dbias1" in lib.evo_attn_last_error().decode()
