@@ -445,10 +445,13 @@ __global__ void __launch_bounds__(FwdCfg<D>::kThreads, 1)
         const int np = (int)min((long long)NWG, s1 - a);
         if (wg >= np) {
           // no row for this warpgroup in the segment's last group: keep the shared streamed-bias
-          // ring in step (wait each fill, then release it)
+          // ring in step (wait each fill, then release it). All four warps must have seen the fill
+          // before the release: the producer may refill the slot right away, and a warp still waiting
+          // for the old phase would then see the parity flip twice and wait forever.
           if (streamed) {
             for (int j = 0; j < p.nKT; ++j) {
               ptx::mbar_wait(&bias_full[bslot], bph);
+              ptx::named_bar_sync(1 + wg, 128);
               if (tid_wg == 0) ptx::mbar_arrive(&bias_empty[bslot]);
               if (++bslot == p.nbias_slots) { bslot = 0; bph ^= 1; }
             }
@@ -594,6 +597,7 @@ __global__ void __launch_bounds__(FwdCfg<D>::kThreads, 1)
         // a warpgroup with no row in this segment still owes its release: wait for the fill first
         if (!released) {
           for (int s2 = 0; s2 < p.nKT; ++s2) ptx::mbar_wait(&bias_full[s2], bph);
+          ptx::named_bar_sync(1 + wg, 128);  // every warp saw the fills before they are released
           if (tid_wg == 0)
             for (int s2 = 0; s2 < p.nKT; ++s2) ptx::mbar_arrive(&bias_empty[s2]);
         }

@@ -215,3 +215,25 @@ def test_dbias1_request_needs_descriptor_flag():
                           p(db2), 0, p(ws), wsb, torch.cuda.current_stream().cuda_stream)
     assert st == N.EVO_ERR_VALIDATION
     assert "need_dbias1" in lib.evo_attn_last_error().decode()
+
+
+def test_fwd_streamed_bias_flat_split_segments():
+    # L = 1024 streams the pair bias through a 3-slot ring shared by the warpgroups; H = 5 makes the
+    # grid a flat item split, so CTAs cross segment boundaries with partial row groups (a warpgroup
+    # with no row keeps the ring in step). Regression: a lagging warp of such a warpgroup missed a
+    # ring phase and hung (C5); repeated launches give the race a chance.
+    import paper_2310_04610_b200 as E
+    from tests.util import O
+
+    Bo, Nr, L, H, D = 1, 24, 1024, 5, 32
+    q, k, v, _, b1, b2 = make_inputs(Bo, Nr, L, H, D, dtype="bf16", seed=13)
+    t = lambda a: torch.tensor(a, dtype=torch.bfloat16, device="cuda")
+    tq, tk, tv, tb1, tb2 = map(t, (q, k, v, b1, b2))
+    for _ in range(5):
+        o, lse = E.evoformer_attention_forward(tq, tk, tv, tb1, tb2)
+    torch.cuda.synchronize()
+    p = O.Problem(Bo * Nr, L, H, D, fmt=O.F32, Bo=Bo)
+    r = lambda a: a.reshape(-1).astype(np.float64)
+    wo, wl = O.forward(p, r(q), r(k), r(v), r(b1), r(b2))
+    assert nmax_err(o.float().cpu().numpy(), wo.reshape(q.shape)) <= 1e-2
+    assert nmax_err(lse.cpu().numpy(), wl.transpose(1, 0, 2)) <= 1e-2
