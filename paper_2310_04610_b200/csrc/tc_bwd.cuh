@@ -54,9 +54,6 @@ constexpr int kOnes = 16 * 32;                           // 16 x 16 bf16 ones: t
 constexpr int kIdent = 16 * 32;                          // 16 x 16 identity: dBias2 strip += dS I on the tensor pipe
 constexpr uint32_t kStripCol = 256, kDqCol = 448, kDkvCol = 480;
 constexpr uint32_t kDb1Col = 384;
-#ifndef EVO_BWD_QS
-#define EVO_BWD_QS 4
-#endif
 #ifndef EVO_BWD_POLY
 #define EVO_BWD_POLY 0
 #endif
@@ -64,13 +61,16 @@ constexpr uint32_t kDb1Col = 384;
 #define EVO_BWD_EXP 0  // timing experiments only (wrong results), bit mask: 1 no dK/dV MMAs, 2 no dQ MMA, 4 no bias LDS, 8 no P/dS stores
 #endif  // dBias1 column sums (M=64, 16 columns) when requested: chunks of <= 2 q-tiles
 
-template <int D>
+template <int D, bool CH>
 struct Cfg {
   static constexpr int kRowBytes = D * 2;
   static constexpr int kTileQ = kBM * kRowBytes;    // Q or dO tile
   static constexpr int kTileK = kBN * kRowBytes;    // K or V tile
-  static constexpr int kQStages = EVO_BWD_QS;       // (Q, dO, lse, delta) ring: a slot refills only once the
-                                                    // gradient MMAs of its step completed, so depth = TMA slack
+  // (Q, dO, lse, delta) ring: a slot refills only once the gradient MMAs of its step completed, so its
+  // depth is the TMA slack. 4 deep with one fp32 dQ staging tile (C4: 574 vs 651 us at 3 deep); the
+  // chunked variant stages dK/dV partials through the same tiles, and there two staging tiles with a
+  // 3-deep ring win (C5: 44.8 vs 57.6 ms)
+  static constexpr int kQStages = CH ? 3 : 4;
   static constexpr int kDqBufs = kQStages > 3 ? 1 : 2;  // fp32 dQ staging tiles (shared-memory budget)
   static constexpr int kKStages = 2;                // (K, V, bias1 chunk) ring
   static constexpr int kBiasTile = kBM * kBN * 2;   // 16 KB
@@ -182,7 +182,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                const __grid_constant__ CUtensorMap tmB2, const __grid_constant__ CUtensorMap tmdQ,
                const __grid_constant__ CUtensorMap tmdK, const __grid_constant__ CUtensorMap tmdV,
                const Params p) {
-  using C = Cfg<D>;
+  using C = Cfg<D, CH>;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   // ---- shared memory carve-up (all operand tiles 1024-aligned)

@@ -213,9 +213,9 @@ BwdScratch bwd_scratch_layout(const evo_attn_desc* d) {
   return w;
 }
 
-template <int D>
+template <int D, bool CH>
 size_t bwd_smem_bytes(int nQT) {
-  using C = bk::Cfg<D>;
+  using C = bk::Cfg<D, CH>;
   size_t b = 1024;
   b += (size_t)C::kQStages * 2 * C::kTileQ + (size_t)C::kKStages * 2 * C::kTileK + 4 * (size_t)C::kPdsTile;
   b += (size_t)nQT * C::kBiasTile + (size_t)C::kDqBufs * bk::kBM * D * 4;
@@ -282,7 +282,7 @@ evo_status launch_bwd(const evo_attn_desc* d, const Shape& s, const void* dout, 
   p.aug = (s.bias1 != nullptr || s.L % bk::kBN != 0) ? 1 : 0;
   p.aug_c = aug_split(1.0 / (double)s.scale, F16);
   p.nBT = s.bias2 ? p.nQC : 0;  // resident pair-bias tiles
-  const size_t smem = bwd_smem_bytes<D>(p.nBT);
+  const size_t smem = dkv_reduce ? bwd_smem_bytes<D, true>(p.nBT) : bwd_smem_bytes<D, false>(p.nBT);
   if (smem > kMaxSmem) {
     *err = "backward shared-memory budget exceeded";
     return EVO_ERR_UNSUPPORTED;
