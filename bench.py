@@ -448,7 +448,9 @@ def main():
                        "l2": "inputs+outputs larger than L2 (no flush needed)" if ideal_bytes(B_local, L, H, D) > 126e6
                        else "working set smaller than L2 (not flushed)"},
             "peak_mem": {"extra_bytes_per_rank": int(peak_extra), "naive_logits_bytes": naive,
-                         "o_l_plan_bytes": 8 * B_local * H * L + 4 * H * L * L},
+                         "o_l_plan_bytes": 8 * B_local * H * L + 4 * H * L * L,
+                         # the reference attn-bench column (run.cpp:223-234): naive / tiled peak
+                         "reduction_ratio": naive / max(int(peak_extra), 1)},
             "roofline": roofline,
             "cpu_baseline": cpu,
             "e2e": {"value": total_flops / (e2e_ms * 1e-3) / 1e12, "unit": UNIT, "ms_per_step": e2e_ms,
