@@ -10,7 +10,7 @@ from ._native import (CudaError, EvoAttnError, NumericError, UnsupportedError, U
 from .evoformer_attention import (DS4Sci_EvoformerAttention, EvoformerAttentionFunction,
                                   evoformer_attention_backward, evoformer_attention_forward,
                                   last_launch_count, resolved_path)
-from .variants import (AttentionVariant, chunked_forward, layout_from_msa, variant_attention,
+from .variants import (AttentionVariant, chunked_forward, layout_from_msa, variant_attention, variant_forward,
                        variant_from_name)
 
 __all__ = [
@@ -18,5 +18,5 @@ __all__ = [
     "evoformer_attention_backward", "last_launch_count", "resolved_path", "EvoAttnError",
     "ValidationError", "NumericError", "UsageError", "CudaError", "UnsupportedError",
     "AttentionVariant", "variant_attention", "variant_from_name", "layout_from_msa",
-    "chunked_forward",
+    "chunked_forward", "variant_forward",
 ]

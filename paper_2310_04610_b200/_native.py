@@ -26,7 +26,8 @@ class Desc(C.Structure):
     _fields_ = [("Bo", C.c_int64), ("N", C.c_int64), ("L", C.c_int64), ("H", C.c_int64),
                 ("D", C.c_int64), ("dtype", C.c_int), ("scale", C.c_double),
                 ("has_bias1", C.c_int), ("has_bias2", C.c_int), ("dbias_dtype", C.c_int),
-                ("path", C.c_int), ("dbias2_multicast", C.c_void_p), ("need_dbias1", C.c_int)]
+                ("path", C.c_int), ("dbias2_multicast", C.c_void_p), ("need_dbias1", C.c_int),
+                ("axes_swapped", C.c_int)]
 
 
 _lib = None

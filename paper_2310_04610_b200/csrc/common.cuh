@@ -56,10 +56,11 @@ struct Shape {
   float scale_log2;   // scale * log2(e)
   const void* bias1;  // (B, L) or null
   const void* bias2;  // (Bo, H, L, L) or null
+  int swapped;        // 1: q/k/v/o are (L, B, H, D) — the raw msa_col / tri_end layout (Bo == 1)
 };
 
 __device__ __forceinline__ size_t row_off(const Shape& s, int b, int i, int h) {
-  return (((size_t)b * s.L + i) * s.H + h) * (size_t)s.D;
+  return ((s.swapped ? (size_t)i * s.B + b : (size_t)b * s.L + i) * s.H + h) * (size_t)s.D;
 }
 
 }  // namespace evo

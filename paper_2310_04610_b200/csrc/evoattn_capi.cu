@@ -34,6 +34,10 @@ evo_status validate(const evo_attn_desc* d) {
   if (d->dbias_dtype != EVO_F32 && d->dbias_dtype != d->dtype)
     return fail(EVO_ERR_VALIDATION, "dbias_dtype must be EVO_F32 or equal to dtype");
   if (!std::isfinite(d->scale)) return fail(EVO_ERR_NUMERIC, "attention scale must be finite");
+  if (d->axes_swapped != 0 && d->axes_swapped != 1)
+    return fail(EVO_ERR_VALIDATION, "axes_swapped must be 0 or 1");
+  if (d->axes_swapped && d->Bo != 1)
+    return fail(EVO_ERR_VALIDATION, "axes_swapped (raw [L, N, H, D] layout) requires Bo == 1");
   if (d->Bo * d->N > 0x7fffffffLL || d->L > 65535 * 64LL || d->H > 65535)
     return fail(EVO_ERR_UNSUPPORTED, "extents exceed the kernels' index range");
   return EVO_OK;
@@ -61,6 +65,7 @@ evo::Shape make_shape(const evo_attn_desc* d, const void* b1, const void* b2) {
   s.scale_log2 = (float)(d->scale * 1.4426950408889634);
   s.bias1 = b1;
   s.bias2 = b2;
+  s.swapped = d->axes_swapped;
   return s;
 }
 
@@ -213,6 +218,8 @@ evo_status evo_attn_bwd(const evo_attn_desc* d, const void* dout, const void* q,
   g_err.clear();
   evo_status st = validate(d);
   if (st) return st;
+  if (d->axes_swapped)
+    return fail(EVO_ERR_UNSUPPORTED, "the backward takes canonical [Bo, N, L, H, D] tensors (axes_swapped = 0)");
   if (!dout || !q || !k || !v || !o || !lse || !dq || !dk || !dv)
     return fail(EVO_ERR_VALIDATION, "dout, q, k, v, o, lse, dq, dk, dv must be non-null");
   if (d->has_bias1 != (bias1 != nullptr)) return fail(EVO_ERR_VALIDATION, "bias1 presence does not match the descriptor");

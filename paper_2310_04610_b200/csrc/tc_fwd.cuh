@@ -53,6 +53,7 @@ enum BiasMode : int { kBiasNone = 0, kBiasResident = 1, kBiasStreamed = 2, kBias
 
 struct FwdParams {
   int B, N, L, H, Bo;
+  int swapped;       // 1: o is [L, B, H, D] (raw msa_col / tri_end layout)
   int nQT, nKT;
   long long total;   // work items = Bo*H*nQT*N
   int aligned;       // 1: CTA c owns part c%split of unit c/split; 0: flat contiguous split
@@ -587,7 +588,8 @@ __global__ void __launch_bounds__(FwdCfg<D>::kThreads, 1)
             const float o0 = __uint_as_float(ov[d]) * inv, o1 = __uint_as_float(ov[d + 1]) * inv;
             ow[d / 2] = F16 ? ptx::pack_f16(o0, o1) : ptx::pack_bf16(o0, o1);
           }
-          uint4* dst = (uint4*)((uint16_t*)p.o + (((size_t)b * p.L + i) * p.H + si.h) * D);
+          uint4* dst = (uint4*)((uint16_t*)p.o +
+                                 ((p.swapped ? (size_t)i * p.B + b : (size_t)b * p.L + i) * p.H + si.h) * D);
 #pragma unroll
           for (int v = 0; v < D / 8; ++v) dst[v] = make_uint4(ow[4 * v], ow[4 * v + 1], ow[4 * v + 2], ow[4 * v + 3]);
           p.lse[((size_t)b * p.H + si.h) * p.L + i] = l_run > 0.f ? (m_run + __log2f(l_run)) * kLn2 : -INFINITY;

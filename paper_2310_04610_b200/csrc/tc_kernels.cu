@@ -49,8 +49,10 @@ CUtensorMapSwizzle swz(int row_bytes) {
 bool map_bl_hd(CUtensorMap* m, const void* base, const Shape& s, int rows, CUtensorMapDataType dt,
                int esize, std::string* err) {
   cuuint64_t dims[4] = {(cuuint64_t)s.D, (cuuint64_t)s.H, (cuuint64_t)s.L, (cuuint64_t)s.B};
-  cuuint64_t strides[3] = {(cuuint64_t)s.D * esize, (cuuint64_t)s.H * s.D * esize,
-                           (cuuint64_t)s.L * s.H * s.D * esize};
+  // swapped (raw msa_col / tri_end layout, (L, B, H, D)): the L and B strides trade places
+  const cuuint64_t hd = (cuuint64_t)s.H * s.D * esize;
+  cuuint64_t strides[3] = {(cuuint64_t)s.D * esize, s.swapped ? hd * (cuuint64_t)s.B : hd,
+                           s.swapped ? hd : hd * (cuuint64_t)s.L};
   cuuint32_t box[4] = {(cuuint32_t)s.D, 1, (cuuint32_t)rows, 1};
   cuuint32_t es[4] = {1, 1, 1, 1};
   CUresult r = encode_fn()(m, dt, 4, const_cast<void*>(base), dims, strides, box, es,
@@ -124,6 +126,7 @@ evo_status launch_fwd(const evo_attn_desc* d, const Shape& s, const void* q, con
     return EVO_ERR_CUDA;
   FwdParams p{};
   p.B = s.B; p.N = s.N; p.L = s.L; p.H = s.H; p.Bo = (int)d->Bo;
+  p.swapped = s.swapped;
   p.nQT = (s.L + kBM - 1) / kBM;
   p.nKT = (s.L + kBN - 1) / kBN;
   p.total = (long long)p.Bo * p.H * p.nQT * p.N;

@@ -16,6 +16,10 @@ outputs and gradients are transposed back, so a caller sees the reference's sema
 axes. bias is the reference's (H, L, L) pair bias (broadcast over B); mask is the DS4Sci bias1
 extension, (B, L) in canonical axes — additive, 0 or a large negative value.
 
+`variant_forward` is the copy-free inference forward: for msa_col / tri_end the kernels read Q/K/V and
+write O in the raw layout through the descriptor's `axes_swapped` strides (TMA maps with the L and
+B strides traded), so no transposed copy is made.
+
 `chunked_forward` is the inference mode: the forward over row chunks with one output buffer, so
 the kernels' per-call working set is bounded by the chunk (rows are independent in the forward).
 """
@@ -28,7 +32,8 @@ from typing import NamedTuple, Optional, Tuple
 import torch
 
 from . import _native as N
-from .evoformer_attention import EvoformerAttentionFunction, evoformer_attention_forward
+from .evoformer_attention import (_DT, _PATHS, _ptr, _stream, EvoformerAttentionFunction,
+                                  evoformer_attention_forward)
 
 
 class AttentionVariant(enum.Enum):
@@ -134,6 +139,36 @@ def variant_attention(variant, q: torch.Tensor, k: torch.Tensor, v: torch.Tensor
     o = EvoformerAttentionFunction.apply(qc.contiguous().unsqueeze(0), kc.contiguous().unsqueeze(0),
                                          vc.contiguous().unsqueeze(0), b1, b2)
     return o.squeeze(0).permute(*inverse_permutation(perm))
+
+
+@torch.no_grad()
+def variant_forward(variant, q: torch.Tensor, k: torch.Tensor, v: torch.Tensor,
+                    bias: Optional[torch.Tensor] = None, mask: Optional[torch.Tensor] = None,
+                    path: str = "auto") -> Tuple[torch.Tensor, torch.Tensor]:
+    """Inference forward of one variant on raw (model-axis) contiguous Q/K/V with no layout copy.
+    Returns (O in the raw axes, LSE [B, H, L] canonical fp32)."""
+    variant = _as_variant(variant)
+    swap = variant in (AttentionVariant.MsaColumnWise, AttentionVariant.TriangularEndNode)
+    perm = _SWAP if swap else _IDENT
+    qc, kc, vc = (t.permute(*perm) for t in (q, k, v))
+    validate_variant_problem(variant, qc, kc, vc, bias, mask)
+    for t in (q, k, v, bias, mask):
+        if t is not None and (not t.is_cuda or not t.is_contiguous()):
+            raise N.ValidationError("inputs must be contiguous CUDA tensors")
+    if q.dtype not in _DT:
+        raise N.ValidationError(f"unsupported dtype {q.dtype}")
+    B, L, H, D = qc.shape
+    lib = N.load()
+    d = N.Desc(1, B, L, H, D, _DT[q.dtype], 1.0 / math.sqrt(D), int(mask is not None),
+               int(bias is not None), N.EVO_F32, _PATHS[path])
+    d.axes_swapped = int(swap)
+    o = torch.empty_like(q)
+    lse = torch.empty((B, H, L), device=q.device, dtype=torch.float32)
+    wsb = lib.evo_attn_fwd_workspace_size(d)
+    ws = torch.empty(max(wsb, 1), device=q.device, dtype=torch.uint8)
+    N.check(lib.evo_attn_fwd(d, _ptr(q), _ptr(k), _ptr(v), _ptr(mask), _ptr(bias), _ptr(o),
+                             _ptr(lse), _ptr(ws), wsb, _stream()))
+    return o, lse
 
 
 @torch.no_grad()

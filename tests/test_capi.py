@@ -75,6 +75,14 @@ def test_status_codes_without_gpu():
     st = lib.evo_attn_bwd(_desc(dbias_dtype=N.EVO_BF16), 1, 1, 1, 1, 1, 1, 1, 1, 1, 1, 1, None, 1,
                           1, 1, 10**9, None)
     assert st == N.EVO_ERR_VALIDATION  # accumulate requires fp32 dbias
+    # raw (axes-swapped) layout: one outer batch only, forward only
+    st = lib.evo_attn_fwd(_desc(Bo=2, axes_swapped=1), 1, 1, 1, 1, 1, 1, 1, None, 0, None)
+    assert st == N.EVO_ERR_VALIDATION and "Bo == 1" in lib.evo_attn_last_error().decode()
+    st = lib.evo_attn_fwd(_desc(axes_swapped=2), 1, 1, 1, 1, 1, 1, 1, None, 0, None)
+    assert st == N.EVO_ERR_VALIDATION
+    st = lib.evo_attn_bwd(_desc(axes_swapped=1), 1, 1, 1, 1, 1, 1, 1, 1, 1, 1, 1, None, 1,
+                          0, 1, 10**9, None)
+    assert st == N.EVO_ERR_UNSUPPORTED
 
 
 def test_simt_path_for_fp32():
