@@ -75,12 +75,12 @@ typedef struct {
                              tcgen05 backward then splits the query axis into chunks of 2 tiles and
                              reduces dK/dV in fp32); a dbias1 request with need_dbias1 == 0 is a
                              ValidationError. The reference has no bias1: 0 there. */
-  int axes_swapped;       /* forward: 1 = q, k, v, o are [L, N, H, D] — the raw MSA-column /
-                             triangle-end-node layout whose attended axis is axis 0
+  int axes_swapped;       /* 1 = q, k, v, o (and do, dq, dk, dv) are [L, N, H, D] — the raw
+                             MSA-column / triangle-end-node layout whose attended axis is axis 0
                              (layout_from_msa, attention.cpp:109-119) — read and written in place
                              through the strides, no transposed copy. Requires Bo == 1; bias1, bias2,
-                             lse stay canonical ([N, L], [H, L, L], [N, H, L]). The backward takes
-                             canonical tensors only (1 there is EVO_ERR_UNSUPPORTED). 0 = canonical. */
+                             lse and the dbias outputs stay canonical ([N, L], [H, L, L], [N, H, L]).
+                             0 = canonical [Bo, N, L, H, D]. */
 } evo_attn_desc;
 
 size_t evo_attn_fwd_workspace_size(const evo_attn_desc* desc);

@@ -218,8 +218,6 @@ evo_status evo_attn_bwd(const evo_attn_desc* d, const void* dout, const void* q,
   g_err.clear();
   evo_status st = validate(d);
   if (st) return st;
-  if (d->axes_swapped)
-    return fail(EVO_ERR_UNSUPPORTED, "the backward takes canonical [Bo, N, L, H, D] tensors (axes_swapped = 0)");
   if (!dout || !q || !k || !v || !o || !lse || !dq || !dk || !dv)
     return fail(EVO_ERR_VALIDATION, "dout, q, k, v, o, lse, dq, dk, dv must be non-null");
   if (d->has_bias1 != (bias1 != nullptr)) return fail(EVO_ERR_VALIDATION, "bias1 presence does not match the descriptor");

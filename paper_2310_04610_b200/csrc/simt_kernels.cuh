@@ -117,15 +117,15 @@ __global__ void delta_kernel(Shape s, const T* __restrict__ dout, const T* __res
   const size_t rows = (size_t)s.B * s.L * s.H;
   for (size_t r = blockIdx.x * (size_t)blockDim.x + threadIdx.x; r < rows;
        r += (size_t)gridDim.x * blockDim.x) {
-    const T* a = dout + r * s.D;
-    const T* c = o + r * s.D;
-    float acc = 0.f;
-    for (int d = 0; d < s.D; ++d) acc = fmaf(to_f(a[d]), to_f(c[d]), acc);
     // r enumerates (b, i, h); delta is stored (b, h, i)
     const int h = (int)(r % s.H);
     const size_t bi = r / s.H;
     const int i = (int)(bi % s.L);
     const size_t b = bi / s.L;
+    const T* a = dout + row_off(s, (int)b, i, h);
+    const T* c = o + row_off(s, (int)b, i, h);
+    float acc = 0.f;
+    for (int d = 0; d < s.D; ++d) acc = fmaf(to_f(a[d]), to_f(c[d]), acc);
     delta[(b * s.H + h) * s.L + i] = acc;
   }
 }

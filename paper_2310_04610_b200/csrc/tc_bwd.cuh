@@ -80,6 +80,7 @@ struct Cfg {
 
 struct Params {
   int B, N, L, H, Bo;
+  int swapped;  // 1: q/k/v/o/dO/dQ/dK/dV are [L, B, H, D] (raw msa_col / tri_end layout)
   int nQT, nKT;
   int nQC, nIC;      // query tiles per chunk (<= 3: the dBias2 strip of a chunk fits TMEM), chunks
   int nBT;           // pair-bias tiles resident in shared memory (nQC, or 0 without bias2)
@@ -705,7 +706,8 @@ __global__ void __launch_bounds__(kThreads, 1)
           for (int d = 0; d < D; d += 2)
             ow[d / 2] = F16 ? ptx::pack_f16(__uint_as_float(v[d]) * sc, __uint_as_float(v[d + 1]) * sc)
                             : ptx::pack_bf16(__uint_as_float(v[d]) * sc, __uint_as_float(v[d + 1]) * sc);
-          uint4* dst = (uint4*)((uint16_t*)(isk ? p.dk : p.dv) + (((size_t)b * p.L + j) * p.H + u.h) * D);
+          uint4* dst = (uint4*)((uint16_t*)(isk ? p.dk : p.dv) +
+                                   ((p.swapped ? (size_t)j * p.B + b : (size_t)b * p.L + j) * p.H + u.h) * D);
 #pragma unroll
           for (int q = 0; q < D / 8; ++q) dst[q] = make_uint4(ow[4 * q], ow[4 * q + 1], ow[4 * q + 2], ow[4 * q + 3]);
         }
@@ -728,7 +730,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 template <int D, typename T>
 __global__ void prep_kernel(const T* __restrict__ dout, const T* __restrict__ o, const float* __restrict__ lse,
                             float* __restrict__ lse2, float* __restrict__ delta_p, int B, int L, int H, int Lp,
-                            float4* __restrict__ zero, long long nzero4) {
+                            float4* __restrict__ zero, long long nzero4, int swapped) {
   ptx::pdl_launch_dependents();
   for (long long x = blockIdx.x * (long long)blockDim.x + threadIdx.x; x < nzero4; x += (long long)gridDim.x * blockDim.x)
     zero[x] = make_float4(0.f, 0.f, 0.f, 0.f);  // fp32 gradient accumulators of the main kernel
@@ -744,8 +746,9 @@ __global__ void prep_kernel(const T* __restrict__ dout, const T* __restrict__ o,
       delta_p[orow] = 0.f;
       continue;
     }
-    const uint4* a4 = (const uint4*)(dout + (((size_t)b * L + i) * H + h) * D);
-    const uint4* b4 = (const uint4*)(o + (((size_t)b * L + i) * H + h) * D);
+    const size_t r = ((swapped ? (size_t)i * B + b : (size_t)b * L + i) * H + h) * D;
+    const uint4* a4 = (const uint4*)(dout + r);
+    const uint4* b4 = (const uint4*)(o + r);
     float acc = 0.f;
 #pragma unroll
     for (int c = 0; c < D / 8; ++c) {
@@ -777,16 +780,25 @@ __global__ void pad_rows_kernel(const float* __restrict__ lse, const float* __re
   }
 }
 
+__device__ __forceinline__ size_t out_off(size_t x, int B, int L, int HD, int swapped) {
+  if (!swapped) return x;
+  const size_t bi = x / (size_t)HD, e = x - bi * (size_t)HD;
+  const size_t b = bi / (size_t)L, i = bi - b * (size_t)L;
+  return (i * (size_t)B + b) * (size_t)HD + e;
+}
+
 // dQ (bf16/f16) = scale * dQacc (fp32); 8 elements per thread and iteration (n % 8 == 0: D >= 16):
 // two 16-byte loads, one 16-byte store
+// acc is canonical [B, L, H, D]; swapped writes the [L, B, H, D] layout (8-element groups stay in one row)
 template <typename T>
-__global__ void dq_convert_kernel(const float* __restrict__ acc, T* __restrict__ dq, size_t n, float scale) {
+__global__ void dq_convert_kernel(const float* __restrict__ acc, T* __restrict__ dq, size_t n, float scale,
+                                  int B, int L, int HD, int swapped) {
   ptx::pdl_wait();  // programmatic dependent of the main kernel
   ptx::pdl_launch_dependents();
   constexpr bool F16 = std::is_same<T, __half>::value;
   if (((uintptr_t)dq & 15) != 0) {  // caller buffer not 16-byte aligned: element stores
     for (size_t x = blockIdx.x * (size_t)blockDim.x + threadIdx.x; x < n; x += (size_t)gridDim.x * blockDim.x)
-      dq[x] = from_f<T>(acc[x] * scale);
+      dq[out_off(x, B, L, HD, swapped)] = from_f<T>(acc[x] * scale);
     return;
   }
   for (size_t x = (blockIdx.x * (size_t)blockDim.x + threadIdx.x) * 8; x < n; x += (size_t)gridDim.x * blockDim.x * 8) {
@@ -796,7 +808,7 @@ __global__ void dq_convert_kernel(const float* __restrict__ acc, T* __restrict__
     w.y = F16 ? ptx::pack_f16(a.z * scale, a.w * scale) : ptx::pack_bf16(a.z * scale, a.w * scale);
     w.z = F16 ? ptx::pack_f16(c.x * scale, c.y * scale) : ptx::pack_bf16(c.x * scale, c.y * scale);
     w.w = F16 ? ptx::pack_f16(c.z * scale, c.w * scale) : ptx::pack_bf16(c.z * scale, c.w * scale);
-    *(uint4*)(dq + x) = w;
+    *(uint4*)(dq + out_off(x, B, L, HD, swapped)) = w;
   }
 }
 

@@ -47,12 +47,13 @@ CUtensorMapSwizzle swz(int row_bytes) {
 
 // (B, L, H, D) row-major as a 4-D map (D, H, L, B); box (D, 1, rows, 1).
 bool map_bl_hd(CUtensorMap* m, const void* base, const Shape& s, int rows, CUtensorMapDataType dt,
-               int esize, std::string* err) {
+               int esize, std::string* err, bool canonical = false) {
+  const bool swapped = s.swapped && !canonical;
   cuuint64_t dims[4] = {(cuuint64_t)s.D, (cuuint64_t)s.H, (cuuint64_t)s.L, (cuuint64_t)s.B};
   // swapped (raw msa_col / tri_end layout, (L, B, H, D)): the L and B strides trade places
   const cuuint64_t hd = (cuuint64_t)s.H * s.D * esize;
-  cuuint64_t strides[3] = {(cuuint64_t)s.D * esize, s.swapped ? hd * (cuuint64_t)s.B : hd,
-                           s.swapped ? hd : hd * (cuuint64_t)s.L};
+  cuuint64_t strides[3] = {(cuuint64_t)s.D * esize, swapped ? hd * (cuuint64_t)s.B : hd,
+                           swapped ? hd : hd * (cuuint64_t)s.L};
   cuuint32_t box[4] = {(cuuint32_t)s.D, 1, (cuuint32_t)rows, 1};
   cuuint32_t es[4] = {1, 1, 1, 1};
   CUresult r = encode_fn()(m, dt, 4, const_cast<void*>(base), dims, strides, box, es,
@@ -246,19 +247,20 @@ evo_status launch_bwd(const evo_attn_desc* d, const Shape& s, const void* dout, 
   float* dkacc = (float*)(ws + w.dk);
   float* dvacc = (float*)(ws + w.dv);
   if (dkv_reduce) {
-    if (!map_bl_hd(&tdk, dkacc, s, bk::kBN, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, err) ||
-        !map_bl_hd(&tdv, dvacc, s, bk::kBN, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, err))
+    if (!map_bl_hd(&tdk, dkacc, s, bk::kBN, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, err, true) ||
+        !map_bl_hd(&tdv, dvacc, s, bk::kBN, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, err, true))
       return EVO_ERR_CUDA;
   } else {
     tdk = tdv = tb;
   }
   if (!map_bl_hd(&tq, q, s, bk::kBM, dt, 2, err) || !map_bl_hd(&tk, k, s, bk::kBN, dt, 2, err) ||
       !map_bl_hd(&tv, v, s, bk::kBN, dt, 2, err) || !map_bl_hd(&tdo, dout, s, bk::kBM, dt, 2, err) ||
-      !map_bl_hd(&tdq, dqacc, s, bk::kBM, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, err))
+      !map_bl_hd(&tdq, dqacc, s, bk::kBM, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, err, true))
     return EVO_ERR_CUDA;
   if (s.bias2 && !map_bias(&tb, s.bias2, s, (int)d->Bo, dt, err)) return EVO_ERR_CUDA;
   bk::Params p{};
   p.B = s.B; p.N = s.N; p.L = s.L; p.H = s.H; p.Bo = (int)d->Bo;
+  p.swapped = s.swapped;
   p.nQT = (s.L + bk::kBM - 1) / bk::kBM;
   p.nKT = (s.L + bk::kBN - 1) / bk::kBN;
   p.nQC = bwd_chunk(d, want_db1);
@@ -301,7 +303,7 @@ evo_status launch_bwd(const evo_attn_desc* d, const Shape& s, const void* dout, 
         lse, delta, lse2, delta_p, s.L, Lp, prow, zero4, nzero4);
   } else {
     bk::prep_kernel<D, T><<<(unsigned)std::min<long long>((prow * Lp + 255) / 256, 148 * 32), 256, 0, st>>>(
-        (const T*)dout, (const T*)o, lse, lse2, delta_p, s.B, s.L, s.H, Lp, zero4, nzero4);
+        (const T*)dout, (const T*)o, lse, lse2, delta_p, s.B, s.L, s.H, Lp, zero4, nzero4, s.swapped);
   }
   ++*launches;
   auto kern = dkv_reduce ? bk::bwd_kernel<D, F16, true> : bk::bwd_kernel<D, F16, false>;
@@ -342,7 +344,7 @@ evo_status launch_bwd(const evo_attn_desc* d, const Shape& s, const void* dout, 
     cfg.stream = st;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    cudaLaunchKernelEx(&cfg, bk::dq_convert_kernel<T>, acc, (T*)out, n, scale);
+    cudaLaunchKernelEx(&cfg, bk::dq_convert_kernel<T>, acc, (T*)out, n, scale, s.B, s.L, s.H * D, s.swapped);
     ++*launches;
   };
   convert(dqacc, dq, s.scale);

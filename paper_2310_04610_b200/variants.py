@@ -11,9 +11,9 @@ Mirrors the reference's variant layer:
 Raw inputs arrive in the model's own axes: MSA variants as (N_msa, N_res, H, D), triangular as
 (N_res, N_res, H, D). Row-wise and start-node attend over axis 1 (canonical as-is); column-wise
 and end-node attend over axis 0, so their canonical (B, L, H, D) view swaps axes 0 and 1
-(attention.cpp:109-119). The swap is a device transpose into the canonical layout the kernels read;
-outputs and gradients are transposed back, so a caller sees the reference's semantics in its own
-axes. bias is the reference's (H, L, L) pair bias (broadcast over B); mask is the DS4Sci bias1
+(attention.cpp:109-119). The kernels take that layout in place (descriptor `axes_swapped`: the TMA
+maps trade the L and B strides; O, dQ, dK, dV are written back in the raw layout), so no transposed
+copy is made in either direction and a caller sees the reference's semantics in its own axes. bias is the reference's (H, L, L) pair bias (broadcast over B); mask is the DS4Sci bias1
 extension, (B, L) in canonical axes — additive, 0 or a large negative value.
 
 `variant_forward` is the copy-free inference forward: for msa_col / tri_end the kernels read Q/K/V and
@@ -130,15 +130,67 @@ def variant_attention(variant, q: torch.Tensor, k: torch.Tensor, v: torch.Tensor
     """Biased axial attention of one variant on raw (model-axis) Q/K/V; differentiable in Q, K, V,
     bias and mask. Returns O in the raw axes. Scale is 1/sqrt(D) (attention.cpp:43-45)."""
     variant = _as_variant(variant)
-    perm = _SWAP if variant in (AttentionVariant.MsaColumnWise, AttentionVariant.TriangularEndNode) else _IDENT
+    swap = variant in (AttentionVariant.MsaColumnWise, AttentionVariant.TriangularEndNode)
+    perm = _SWAP if swap else _IDENT
     qc, kc, vc = (t.permute(*perm) for t in (q, k, v))
     validate_variant_problem(variant, qc, kc, vc, bias, mask)
-    B, L, H, D = qc.shape
-    b1 = None if mask is None else mask.reshape(1, B, 1, 1, L)
-    b2 = None if bias is None else bias.reshape(1, 1, H, L, L)
-    o = EvoformerAttentionFunction.apply(qc.contiguous().unsqueeze(0), kc.contiguous().unsqueeze(0),
-                                         vc.contiguous().unsqueeze(0), b1, b2)
-    return o.squeeze(0).permute(*inverse_permutation(perm))
+    if not all(t.is_cuda for t in (q, k, v, bias, mask) if t is not None):
+        raise N.ValidationError("inputs must be CUDA tensors")
+    return _VariantFunction.apply(q.contiguous(), k.contiguous(), v.contiguous(),
+                                  None if mask is None else mask.contiguous(),
+                                  None if bias is None else bias.contiguous(), swap)
+
+
+def _desc(q, B, L, H, D, mask, bias, swap, path="auto", dbias_dtype=None):
+    if q.dtype not in _DT:
+        raise N.ValidationError(f"unsupported dtype {q.dtype}")
+    d = N.Desc(1, B, L, H, D, _DT[q.dtype], 1.0 / math.sqrt(D), int(mask is not None),
+               int(bias is not None), _DT[dbias_dtype] if dbias_dtype is not None else N.EVO_F32,
+               _PATHS[path])
+    d.axes_swapped = int(swap)
+    return d
+
+
+def _dims(q, swap):
+    A0, A1, H, D = q.shape
+    return (A1, A0, H, D) if swap else (A0, A1, H, D)
+
+
+class _VariantFunction(torch.autograd.Function):
+    """Raw-layout autograd: forward and backward both read/write the model's axes in place."""
+
+    @staticmethod
+    def forward(ctx, q, k, v, mask, bias, swap):
+        B, L, H, D = _dims(q, swap)
+        lib = N.load()
+        d = _desc(q, B, L, H, D, mask, bias, swap)
+        o = torch.empty_like(q)
+        lse = torch.empty((B, H, L), device=q.device, dtype=torch.float32)
+        wsb = lib.evo_attn_fwd_workspace_size(d)
+        ws = torch.empty(max(wsb, 1), device=q.device, dtype=torch.uint8)
+        N.check(lib.evo_attn_fwd(d, _ptr(q), _ptr(k), _ptr(v), _ptr(mask), _ptr(bias), _ptr(o),
+                                 _ptr(lse), _ptr(ws), wsb, _stream()))
+        ctx.save_for_backward(q, k, v, o, lse, mask, bias)
+        ctx.swap = swap
+        return o
+
+    @staticmethod
+    def backward(ctx, grad_o):
+        q, k, v, o, lse, mask, bias = ctx.saved_tensors
+        swap = ctx.swap
+        B, L, H, D = _dims(q, swap)
+        lib = N.load()
+        d = _desc(q, B, L, H, D, mask, bias, swap, dbias_dtype=q.dtype)
+        db1 = torch.empty_like(mask) if mask is not None and ctx.needs_input_grad[3] else None
+        db2 = torch.empty_like(bias) if bias is not None and ctx.needs_input_grad[4] else None
+        d.need_dbias1 = int(db1 is not None)
+        dq, dk, dv = torch.empty_like(q), torch.empty_like(q), torch.empty_like(q)
+        wsb = lib.evo_attn_bwd_workspace_size(d)
+        ws = torch.empty(max(wsb, 1), device=q.device, dtype=torch.uint8)
+        N.check(lib.evo_attn_bwd(d, _ptr(grad_o.contiguous()), _ptr(q), _ptr(k), _ptr(v), _ptr(mask),
+                                 _ptr(bias), _ptr(o), _ptr(lse), _ptr(dq), _ptr(dk), _ptr(dv),
+                                 _ptr(db1), _ptr(db2), 0, _ptr(ws), wsb, _stream()))
+        return dq, dk, dv, db1, db2, None
 
 
 @torch.no_grad()
@@ -155,13 +207,9 @@ def variant_forward(variant, q: torch.Tensor, k: torch.Tensor, v: torch.Tensor,
     for t in (q, k, v, bias, mask):
         if t is not None and (not t.is_cuda or not t.is_contiguous()):
             raise N.ValidationError("inputs must be contiguous CUDA tensors")
-    if q.dtype not in _DT:
-        raise N.ValidationError(f"unsupported dtype {q.dtype}")
     B, L, H, D = qc.shape
     lib = N.load()
-    d = N.Desc(1, B, L, H, D, _DT[q.dtype], 1.0 / math.sqrt(D), int(mask is not None),
-               int(bias is not None), N.EVO_F32, _PATHS[path])
-    d.axes_swapped = int(swap)
+    d = _desc(q, B, L, H, D, mask, bias, swap, path)
     o = torch.empty_like(q)
     lse = torch.empty((B, H, L), device=q.device, dtype=torch.float32)
     wsb = lib.evo_attn_fwd_workspace_size(d)

@@ -80,9 +80,9 @@ def test_status_codes_without_gpu():
     assert st == N.EVO_ERR_VALIDATION and "Bo == 1" in lib.evo_attn_last_error().decode()
     st = lib.evo_attn_fwd(_desc(axes_swapped=2), 1, 1, 1, 1, 1, 1, 1, None, 0, None)
     assert st == N.EVO_ERR_VALIDATION
-    st = lib.evo_attn_bwd(_desc(axes_swapped=1), 1, 1, 1, 1, 1, 1, 1, 1, 1, 1, 1, None, 1,
+    st = lib.evo_attn_bwd(_desc(Bo=2, axes_swapped=1), 1, 1, 1, 1, 1, 1, 1, 1, 1, 1, 1, None, 1,
                           0, 1, 10**9, None)
-    assert st == N.EVO_ERR_UNSUPPORTED
+    assert st == N.EVO_ERR_VALIDATION
 
 
 def test_simt_path_for_fp32():

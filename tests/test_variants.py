@@ -79,6 +79,8 @@ def _variant_case(variant, raw_shape, dtype="bf16", seed=3):
     ("msa_col", (64, 96, 4, 32)),       # attends over N_msa = 64 for each of 96 residues
     ("tri_start", (96, 96, 2, 32)),
     ("tri_end", (96, 96, 2, 32)),
+    ("tri_end", (100, 100, 2, 32)),     # L % 8 != 0: SIMT backward in the raw layout
+    ("msa_col", (200, 24, 2, 16)),      # ragged tiles, D 16
 ])
 def test_variant_parity(variant, raw_shape, cuda):
     raw, b1, b2, want, to_raw = _variant_case(variant, raw_shape)
@@ -141,3 +143,26 @@ def test_variant_forward_in_place_layout(variant, raw_shape, path, cuda):
     # same numbers as the transposing autograd path
     o2 = Vr.variant_attention(variant, q, k, v, bias, mask)
     assert (o.float() - o2.float()).abs().max().item() <= 2e-2 * o2.float().abs().max().item()
+
+
+@pytest.mark.gpu
+def test_variant_msa_col_mask_grad_chunked(cuda):
+    """msa_col in the raw layout with a mask gradient: the tcgen05 backward splits the query axis
+    (L = 320, three tiles -> chunks of two), reduces dK/dV in canonical fp32 accumulators and the
+    conversion writes them back in the raw layout."""
+    A0, A1, H, D = 320, 16, 2, 32
+    q, k, v, do, b1, _ = make_inputs(1, A1, A0, H, D, dtype="bf16", bias1=True, bias2=False, seed=9)
+    want = oracle_fwd_bwd(q, k, v, do, b1, None, need_dbias1=True)
+    to_raw = lambda a: a[0].transpose(1, 0, 2, 3)
+    dev = lambda a: torch.tensor(np.ascontiguousarray(a), dtype=torch.bfloat16, device="cuda")
+    tq, tk, tv, tdo = (dev(to_raw(a)).requires_grad_(i < 3) for i, a in enumerate((q, k, v, do)))
+    mask = dev(b1.reshape(A1, A0)).requires_grad_(True)
+    o = Vr.variant_attention("msa_col", tq, tk, tv, None, mask)
+    o.backward(tdo)
+    torch.cuda.synchronize()
+    f = lambda t: t.detach().float().cpu().numpy()
+    wo, _, wdq, wdk, wdv, wdb1, _ = want
+    errs = {"O": nmax_err(f(o), to_raw(wo)), "dQ": nmax_err(f(tq.grad), to_raw(wdq)),
+            "dK": nmax_err(f(tk.grad), to_raw(wdk)), "dV": nmax_err(f(tv.grad), to_raw(wdv)),
+            "dBias1": nmax_err(f(mask.grad), wdb1.reshape(A1, A0))}
+    assert max(errs.values()) <= TOL["bf16"], errs
