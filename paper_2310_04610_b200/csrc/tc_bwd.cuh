@@ -80,7 +80,6 @@ struct Cfg {
 
 struct Params {
   int B, N, L, H, Bo;
-  int swapped;  // 1: q/k/v/o/dO/dQ/dK/dV are [L, B, H, D] (raw msa_col / tri_end layout)
   int nQT, nKT;
   int nQC, nIC;      // query tiles per chunk (<= 3: the dBias2 strip of a chunk fits TMEM), chunks
   int nBT;           // pair-bias tiles resident in shared memory (nQC, or 0 without bias2)
@@ -100,6 +99,7 @@ struct Params {
   int aug;             // extra K-step adding bias1 / scale (bias1 present or L % 64 != 0)
   uint32_t aug_c;      // (c_lo << 16) | c_hi: 16-bit split of 1/scale
   unsigned long long* trace;  // bring-up timeline of CTA 0 (null in production)
+  int swapped;  // 1: q/k/v/o/dO/dQ/dK/dV are [L, B, H, D] (raw msa_col / tri_end layout)
 };
 
 // CTA-0 timeline of steps [kTrFirst, kTrFirst + 64): 8 events x 64 steps (bring-up aid)
@@ -176,7 +176,7 @@ __device__ __forceinline__ void red_v4_multimem(float* mc_addr, float a, float b
                : "memory");
 }
 
-template <int D, bool F16, bool CH>  // CH: the query axis is split into chunks (L > 384)
+template <int D, bool F16, bool CH, bool SW>  // CH: the query axis is split into chunks (L > 384); SW: raw [L, B, H, D] layout
 __global__ void __launch_bounds__(kThreads, 1)
     bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
                const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmdO,
@@ -707,7 +707,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             ow[d / 2] = F16 ? ptx::pack_f16(__uint_as_float(v[d]) * sc, __uint_as_float(v[d + 1]) * sc)
                             : ptx::pack_bf16(__uint_as_float(v[d]) * sc, __uint_as_float(v[d + 1]) * sc);
           uint4* dst = (uint4*)((uint16_t*)(isk ? p.dk : p.dv) +
-                                   ((p.swapped ? (size_t)j * p.B + b : (size_t)b * p.L + j) * p.H + u.h) * D);
+                                   ((SW ? (size_t)j * p.B + b : (size_t)b * p.L + j) * p.H + u.h) * D);
 #pragma unroll
           for (int q = 0; q < D / 8; ++q) dst[q] = make_uint4(ow[4 * q], ow[4 * q + 1], ow[4 * q + 2], ow[4 * q + 3]);
         }
@@ -727,10 +727,11 @@ __global__ void __launch_bounds__(kThreads, 1)
 // and lse2 = lse * log2e, both laid out [B, H, Lp] with the rows past L padded (+inf / 0).
 // Thread per (b, i, h): D contiguous elements of dO and O, 16-byte loads (neighbouring threads read
 // neighbouring rows: the dO / O streams, 2/3 of the bytes, are fully contiguous).
-template <int D, typename T>
+template <int D, typename T, bool SW>
 __global__ void prep_kernel(const T* __restrict__ dout, const T* __restrict__ o, const float* __restrict__ lse,
                             float* __restrict__ lse2, float* __restrict__ delta_p, int B, int L, int H, int Lp,
-                            float4* __restrict__ zero, long long nzero4, int swapped) {
+                            float4* __restrict__ zero, long long nzero4) {
+  constexpr bool swapped = SW;
   ptx::pdl_launch_dependents();
   for (long long x = blockIdx.x * (long long)blockDim.x + threadIdx.x; x < nzero4; x += (long long)gridDim.x * blockDim.x)
     zero[x] = make_float4(0.f, 0.f, 0.f, 0.f);  // fp32 gradient accumulators of the main kernel
@@ -790,9 +791,10 @@ __device__ __forceinline__ size_t out_off(size_t x, int B, int L, int HD, int sw
 // dQ (bf16/f16) = scale * dQacc (fp32); 8 elements per thread and iteration (n % 8 == 0: D >= 16):
 // two 16-byte loads, one 16-byte store
 // acc is canonical [B, L, H, D]; swapped writes the [L, B, H, D] layout (8-element groups stay in one row)
-template <typename T>
+template <typename T, bool SW>
 __global__ void dq_convert_kernel(const float* __restrict__ acc, T* __restrict__ dq, size_t n, float scale,
-                                  int B, int L, int HD, int swapped) {
+                                  int B, int L, int HD) {
+  constexpr int swapped = SW;
   ptx::pdl_wait();  // programmatic dependent of the main kernel
   ptx::pdl_launch_dependents();
   constexpr bool F16 = std::is_same<T, __half>::value;

@@ -302,11 +302,13 @@ evo_status launch_bwd(const evo_attn_desc* d, const Shape& s, const void* dout, 
     bk::pad_rows_kernel<<<(unsigned)std::min<long long>((prow * Lp + 255) / 256, 148 * 16), 256, 0, st>>>(
         lse, delta, lse2, delta_p, s.L, Lp, prow, zero4, nzero4);
   } else {
-    bk::prep_kernel<D, T><<<(unsigned)std::min<long long>((prow * Lp + 255) / 256, 148 * 32), 256, 0, st>>>(
-        (const T*)dout, (const T*)o, lse, lse2, delta_p, s.B, s.L, s.H, Lp, zero4, nzero4, s.swapped);
+    auto prep = s.swapped ? bk::prep_kernel<D, T, true> : bk::prep_kernel<D, T, false>;
+    prep<<<(unsigned)std::min<long long>((prow * Lp + 255) / 256, 148 * 32), 256, 0, st>>>(
+        (const T*)dout, (const T*)o, lse, lse2, delta_p, s.B, s.L, s.H, Lp, zero4, nzero4);
   }
   ++*launches;
-  auto kern = dkv_reduce ? bk::bwd_kernel<D, F16, true> : bk::bwd_kernel<D, F16, false>;
+  auto kern = s.swapped ? (dkv_reduce ? bk::bwd_kernel<D, F16, true, true> : bk::bwd_kernel<D, F16, false, true>)
+                        : (dkv_reduce ? bk::bwd_kernel<D, F16, true, false> : bk::bwd_kernel<D, F16, false, false>);
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   const int G = sm_count();
   const long long units = (long long)p.Bo * p.H * p.nKT * p.nIC;
@@ -344,7 +346,8 @@ evo_status launch_bwd(const evo_attn_desc* d, const Shape& s, const void* dout, 
     cfg.stream = st;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    cudaLaunchKernelEx(&cfg, bk::dq_convert_kernel<T>, acc, (T*)out, n, scale, s.B, s.L, s.H * D, s.swapped);
+    cudaLaunchKernelEx(&cfg, s.swapped ? bk::dq_convert_kernel<T, true> : bk::dq_convert_kernel<T, false>, acc,
+                       (T*)out, n, scale, s.B, s.L, s.H * D);
     ++*launches;
   };
   convert(dqacc, dq, s.scale);

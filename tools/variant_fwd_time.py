@@ -44,6 +44,24 @@ def main():
     print(f"tri_end fwd C3: copy-free {t1 * 1e3:.1f} us ({fl / t1 / 1e9:.0f} TFLOP/s), "
           f"transposed {t2 * 1e3:.1f} us ({fl / t2 / 1e9:.0f} TFLOP/s), max |diff| {err:.3g}")
 
+    # fwd+bwd through autograd: raw layout in place vs transposing around the canonical operator
+    qg, kg, vg = (t.clone().requires_grad_(True) for t in (q, k, v))
+    bg = bias.clone().requires_grad_(True)
+    do = r(L, L, H, D)
+
+    def step_raw():
+        Vr.variant_attention("tri_end", qg, kg, vg, bg, mask).backward(do)
+
+    def step_transposed():
+        qc, kc, vc = (t.transpose(0, 1).contiguous().unsqueeze(0) for t in (qg, kg, vg))
+        o = E.DS4Sci_EvoformerAttention(qc, kc, vc, [mask.reshape(1, L, 1, 1, L), bg.reshape(1, 1, H, L, L)])
+        o[0].transpose(0, 1).backward(do)
+
+    t3, t4 = timed(step_raw, 20), timed(step_transposed, 20)
+    fl = 14 * L * H * L * L * D
+    print(f"tri_end fwd+bwd C3: raw layout {t3 * 1e3:.1f} us ({fl / t3 / 1e9:.0f} TFLOP/s), "
+          f"transposed {t4 * 1e3:.1f} us ({fl / t4 / 1e9:.0f} TFLOP/s)")
+
 
 if __name__ == "__main__":
     main()
