@@ -426,6 +426,22 @@ def main():
                            "path": E.resolved_path(qq, bb1, bb2)}
             del qq, kk, vv, dd, bb1, bb2
             torch.cuda.empty_cache()
+        # C3 as the triangle END-node variant: raw [N_res, N_res, H, D] tensors attended over axis 0,
+        # run in place through the variant layer (descriptor axes_swapped; autograd fwd+bwd)
+        Lt, Ht, Dt = 384, 4, 32
+        g = torch.Generator(device=dev).manual_seed(7)
+        rr = lambda *sh: (torch.rand(*sh, device=dev, generator=g) * 2 - 1).to(torch.bfloat16)
+        tq, tk, tv = (rr(Lt, Lt, Ht, Dt).requires_grad_(True) for _ in range(3))
+        tb, tdo = rr(Ht, Lt, Lt).requires_grad_(True), rr(Lt, Lt, Ht, Dt)
+        tm = torch.zeros(Lt, Lt, device=dev, dtype=torch.bfloat16)
+        tri = lambda: E.variant_attention("tri_end", tq, tk, tv, tb, tm).backward(tdo)
+        for _ in range(3):
+            tri()
+        mm = time_call(tri, 20)
+        extra["c3_tri_end_raw_layout"] = {"ms_per_step": mm, "tflops": flops(Lt, Lt, Ht, Dt) / mm / 1e9,
+                                          "path": "tcgen05 (axes_swapped)"}
+        del tq, tk, tv, tb, tdo, tm
+        torch.cuda.empty_cache()
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
