@@ -113,6 +113,21 @@ int evo_attn_last_launch_count(void);
 /* Message of the last error on this thread ("" if none). */
 const char* evo_attn_last_error(void);
 
+/* Host-side synthetic inputs identical to the reference's instance generator (not the hot path):
+ * draws [skip, skip + n) of the stream derived_rng(seed, stream) — SeededRng (std::mt19937_64, top 53
+ * bits; rng.hpp:16-43) — as lo + (hi - lo) * uniform(), rounded RNE to `dtype` exactly like
+ * random_uniform / round_to_format (rng.cpp:5-10, numeric_format.cpp:42-78), into HOST memory.
+ * random_problem (run.cpp:178-189) draws Q, K, V, then the bias from one stream; the harness's dO
+ * comes from stream + 2^20 (run.cpp:194-195). */
+evo_status evo_random_uniform(uint64_t seed, uint64_t stream, int64_t skip, int64_t n, double lo,
+                              double hi, evo_dtype dtype, void* host_out);
+
+/* DS4Sci mask bias1 (no reference counterpart): for rows [row0, row0 + rows) of an [*, L] mask, one
+ * uniform draw per (row, key) of derived_rng(seed, stream); value `neg` where draw < rate, else 0;
+ * key 0 is never masked (no fully masked row). HOST memory, `dtype` elements. */
+evo_status evo_random_mask(uint64_t seed, uint64_t stream, int64_t rows, int64_t row0, int64_t L,
+                           double rate, double neg, evo_dtype dtype, void* host_out);
+
 /* Library version string, e.g. "evoattn 0.1 sm_100a". */
 const char* evo_attn_version(void);
 

@@ -93,6 +93,8 @@ def _reflib():
         _ref.evomem_ref_analytic_bytes.restype = C.c_int64
         _ref.evomem_ref_analytic_bytes.argtypes = [i64, i64, i64, i64, i, i, i, i64, i64, i64]
         _ref.evomem_ref_last_error.restype = C.c_char_p
+        _ref.evomem_ref_random_uniform.restype = C.c_int
+        _ref.evomem_ref_random_uniform.argtypes = [C.c_uint64, C.c_uint64, i64, i64, i, d, d, _dp]
     return _ref
 
 
@@ -244,3 +246,14 @@ def ref_threaded_f32(q, k, v, bias, dout, threads: int, scale=None):
 def ref_analytic_bytes(H, B, L, D, bytes_per_elem, tiled, backward, tile=(64, 64), workers=1):
     return int(_reflib().evomem_ref_analytic_bytes(H, B, L, D, bytes_per_elem, int(tiled),
                                                    int(backward), tile[0], tile[1], workers))
+
+
+def ref_random_uniform(seed: int, stream: int, skip: int, n: int, fmt: str, lo=-1.0, hi=1.0) -> np.ndarray:
+    """The reference's derived_rng + random_uniform (rng.hpp:41-47): n values after `skip` draws."""
+    out = np.zeros(n)
+    f = {"f64": 0, "f32": 1, "bf16": 2, "f16": 3}[fmt]
+    lib = _reflib()
+    st = lib.evomem_ref_random_uniform(seed, stream, skip, n, f, lo, hi, _ptr(out))
+    if st:
+        raise OracleError(st, lib.evomem_ref_last_error().decode())
+    return out

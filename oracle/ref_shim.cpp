@@ -15,6 +15,7 @@
 #include <evomem/errors.hpp>
 #include <evomem/ledger.hpp>
 #include <evomem/memory_model.hpp>
+#include <evomem/rng.hpp>
 
 #include <cstdint>
 #include <cstring>
@@ -194,6 +195,22 @@ int evomem_ref_tiled_threaded_f32(std::int64_t B, std::int64_t L, std::int64_t H
     }
   }
   return 0;
+}
+
+// The reference's own instance generator (rng.hpp:41-47, rng.cpp:5-10): `skip` draws of
+// derived_rng(seed, stream) are consumed, then n values of random_uniform in format `fmt` (values
+// out as doubles). Pins the product-side port (evo_random_uniform) bit for bit.
+int evomem_ref_random_uniform(std::uint64_t seed, std::uint64_t stream, std::int64_t skip, std::int64_t n,
+                              int fmt, double lo, double hi, double* out) {
+  try {
+    SeededRng rng = derived_rng(seed, stream);
+    for (std::int64_t i = 0; i < skip; ++i) rng.next_u64();
+    Tensor t = random_uniform({n}, fmt_of(fmt), rng, lo, hi);
+    copy_out(t, out);
+    return 0;
+  } catch (const std::exception& e) {
+    return status_of(e);
+  }
 }
 
 // memory_model.hpp analytic bytes (naive vs tiled), for the peak-memory report.

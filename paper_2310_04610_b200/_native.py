@@ -18,7 +18,7 @@ EVO_PATH_AUTO, EVO_PATH_SIMT, EVO_PATH_TCGEN05 = 0, 1, 2
 EXPORTED = (
     "evo_attn_fwd_workspace_size", "evo_attn_bwd_workspace_size", "evo_attn_fwd", "evo_attn_bwd",
     "evo_attn_resolved_path", "evo_attn_last_launch_count", "evo_attn_last_error",
-    "evo_attn_version",
+    "evo_attn_version", "evo_random_uniform", "evo_random_mask",
 )
 
 
@@ -62,6 +62,12 @@ def load(build_if_missing: bool = True):
     lib.evo_attn_last_launch_count.restype = C.c_int
     lib.evo_attn_last_error.restype = C.c_char_p
     lib.evo_attn_version.restype = C.c_char_p
+    lib.evo_random_uniform.argtypes = [C.c_uint64, C.c_uint64, C.c_int64, C.c_int64, C.c_double, C.c_double,
+                                       C.c_int, vp]
+    lib.evo_random_uniform.restype = C.c_int
+    lib.evo_random_mask.argtypes = [C.c_uint64, C.c_uint64, C.c_int64, C.c_int64, C.c_int64, C.c_double,
+                                    C.c_double, C.c_int, vp]
+    lib.evo_random_mask.restype = C.c_int
     _lib = lib
     return lib
 

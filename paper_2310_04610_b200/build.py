@@ -20,7 +20,7 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-I", os.path.join(ROOT, "include"),
          "--expt-relaxed-constexpr", "-Xptxas", "-warn-spills"] + os.environ.get("EVO_NVCC_EXTRA", "").split()
-SOURCES = ["evoattn_capi.cu", "tc_kernels.cu"]
+SOURCES = ["evoattn_capi.cu", "tc_kernels.cu", "evoattn_inputs.cu"]
 
 
 def _sources():
@@ -37,16 +37,19 @@ def _needs_rebuild() -> bool:
     return os.path.getmtime(os.path.join(ROOT, "include", "evoattn.h")) > t
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and not _needs_rebuild():
+def build(force: bool = False, verbose: bool = False, out: str = LIB, extra=()) -> str:
+    """Compile csrc/ into `out` (default the in-tree library); `extra` = additional nvcc flags
+    (A/B variants are built into other paths with tools/build_variant.sh)."""
+    if not force and out == LIB and not _needs_rebuild():
         return LIB
     os.makedirs(LIBDIR, exist_ok=True)
     objs = []
     cmds = []
+    tag = os.path.basename(out).replace(".so", "")
     for src in _sources():
-        obj = os.path.join(LIBDIR, src.replace(".cu", ".o"))
+        obj = os.path.join(LIBDIR, f"{tag}_" + src.replace(".cu", ".o"))
         objs.append(obj)
-        cmds.append([NVCC, *ARCH, *FLAGS, "-c", os.path.join(CSRC, src), "-o", obj])
+        cmds.append([NVCC, *ARCH, *FLAGS, *extra, "-c", os.path.join(CSRC, src), "-o", obj])
 
     def run(cmd):
         r = subprocess.run(cmd, capture_output=True, text=True)
@@ -55,14 +58,14 @@ def build(force: bool = False, verbose: bool = False) -> str:
         return r.stderr
 
     with cf.ThreadPoolExecutor(max_workers=len(cmds)) as ex:
-        for out in ex.map(run, cmds):
-            if verbose and out:
-                sys.stderr.write(out)
-    link = [NVCC, *ARCH, "-shared", "-o", LIB, *objs]
+        for log in ex.map(run, cmds):
+            if verbose and log:
+                sys.stderr.write(log)
+    link = [NVCC, *ARCH, "-shared", "-o", out, *objs]
     run(link)
     for o in objs:
         os.remove(o)
-    return LIB
+    return out
 
 
 if __name__ == "__main__":

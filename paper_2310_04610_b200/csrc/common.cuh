@@ -7,6 +7,10 @@
 
 #include "../../include/evoattn.h"
 
+#ifndef EVO_TRACE
+#define EVO_TRACE 0  // bring-up timelines (tools/trace_*.py build with -DEVO_TRACE=1); compiled out otherwise
+#endif
+
 namespace evo {
 
 constexpr float kLog2e = 1.4426950408889634f;

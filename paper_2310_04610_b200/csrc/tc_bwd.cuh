@@ -54,6 +54,9 @@ constexpr int kOnes = 16 * 32;                           // 16 x 16 bf16 ones: t
 constexpr int kIdent = 16 * 32;                          // 16 x 16 identity: dBias2 strip += dS I on the tensor pipe
 constexpr uint32_t kStripCol = 256, kDqCol = 448, kDkvCol = 480;
 constexpr uint32_t kDb1Col = 384;
+#ifndef EVO_BWD_LATE_PDS
+#define EVO_BWD_LATE_PDS 1  // softmax waits for its P/dS buffer only before the first store
+#endif
 #ifndef EVO_BWD_POLY
 #define EVO_BWD_POLY 0
 #endif
@@ -107,7 +110,9 @@ constexpr uint32_t kTrFirst = 100;
 enum BwdTrace { kTbSIssue = 0, kTbSSeen = 1, kTbPds0 = 2, kTbPds1 = 3, kTbGrads = 4, kTbDqSeen = 5, kTbDqOut = 6,
                 kTbQFull = 7, kTbProdQ = 8, kTbKFull = 9, kTbGradsStart = 10, kTbLoopTop = 11 };
 __device__ __forceinline__ void trace(const Params& p, int ev, uint32_t step) {
-  if (p.trace && blockIdx.x == 0 && step - kTrFirst < 64u) p.trace[ev * 64 + (step - kTrFirst)] = clock64();
+  if constexpr (EVO_TRACE) {
+    if (p.trace && blockIdx.x == 0 && step - kTrFirst < 64u) p.trace[ev * 64 + (step - kTrFirst)] = clock64();
+  }
 }
 
 struct Walker {
@@ -472,7 +477,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             trace(p, kTbSIssue, step);
           }
           __syncwarp();
-          if (p.trace && blockIdx.x == 0 && step - kTrFirst < 64u) {  // bring-up: S completion time
+          if (EVO_TRACE && p.trace && blockIdx.x == 0 && step - kTrFirst < 64u) {  // bring-up: S completion time
             ptx::mbar_wait(&s_full[sb], (step >> 1) & 1);
             if (lane == 0) trace(p, kTbLoopTop, step);
           }
@@ -515,7 +520,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           const float2 nd = make_float2(-dl, -dl);
           ptx::mbar_wait(&s_full[sb], ph);
           if (tid_wg == 0 && wg == 0) trace(p, kTbSSeen, step);
-          ptx::mbar_wait(&pds_free[sb], ph ^ 1);  // P/dS buffer sb: MMAs of step-2 done
+          if (!EVO_BWD_LATE_PDS) ptx::mbar_wait(&pds_free[sb], ph ^ 1);  // P/dS buffer sb: MMAs of step-2 done
           ptx::tc_fence_after();
           const uint32_t bt = ptx::smem_u32(sBias + (size_t)(it - (CH ? u.it0 : 0)) * C::kBiasTile) + r * 128;
           const uint32_t pbase = ptx::smem_u32(sP + sb * C::kPdsTile) + r * 128;
@@ -560,7 +565,10 @@ __global__ void __launch_bounds__(kThreads, 1)
                 dk[k / 2] = F16 ? ptx::pack_f16(d.x, d.y) : ptx::pack_bf16(d.x, d.y);
               }
             }
-            // P and dS -> shared (128B swizzle; chunks 2kb, 2kb+1 of row r)
+            // P and dS -> shared (128B swizzle; chunks 2kb, 2kb+1 of row r). The buffer's previous
+            // readers (the gradient MMAs of step - 2) are waited for only now: the first block's
+            // loads and exponentials overlap their tail
+            if (EVO_BWD_LATE_PDS && cb == 0) ptx::mbar_wait(&pds_free[sb], ph ^ 1);
 #pragma unroll
             for (int c = 0; c < ((EVO_BWD_EXP & 8) ? 0 : 2); ++c) {
               const uint32_t off = (uint32_t)((2 * kb + c) << 4) ^ r7;

@@ -73,7 +73,9 @@ struct FwdParams {
 
 enum TraceEv { kTrKV = 0, kTrS = 1, kTrSseen = 2, kTrP0 = 3, kTrP1 = 4, kTrPV = 5, kTrRowEnd = 6, kTrRowStart = 7 };
 __device__ __forceinline__ void trace(const FwdParams& p, int ev, uint32_t tile) {
-  if (p.trace && blockIdx.x == 0 && tile < 64) p.trace[ev * 64 + tile] = clock64();
+  if constexpr (EVO_TRACE) {
+    if (p.trace && blockIdx.x == 0 && tile < 64) p.trace[ev * 64 + tile] = clock64();
+  }
 }
 
 template <bool F16>

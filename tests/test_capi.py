@@ -12,7 +12,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 def _declared():
     src = open(os.path.join(ROOT, "include", "evoattn.h")).read()
-    return sorted(set(re.findall(r"\b(evo_attn_\w+)\s*\(", src)))
+    return sorted(set(re.findall(r"\b(evo_\w+)\s*\(", src)))
 
 
 def test_header_declares_the_boundary():
