@@ -7,10 +7,10 @@ over rows (in-kernel, then NCCL all-reduce across ranks when N > 1).
 Default workload: configs[3] of BASELINE.json — OpenFold finetune MSA row
 attention N_seq=512 N_res=384 H=8 D=32 bf16 — the configuration the north-star
 target (>=50% of dense bf16 peak on 1 B200) is quoted on. --config c1..c5
-selects the others. Multi-GPU (--scaling weak, the default): every rank owns its
-own rows of the configuration (the MSA-row / triangle-start axis partitioned, per
-rank the full config's row count) and the ranks exchange only the fp32 dBias2
-partial (NCCL all-reduce); --scaling strong splits the config's rows over ranks.
+selects the others. Multi-GPU (--scaling strong, the default): the config's rows
+(the MSA-row / triangle-start axis) are split over the ranks and the ranks exchange
+only the fp32 dBias2 partial (NCCL all-reduce); --scaling weak gives every rank a
+full config's rows.
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--config c4] [--impl ours|reference]
   torchrun --nproc-per-node N bench.py --gpus N ...
@@ -123,60 +123,88 @@ class ClockSampler:
                 "samples": len(sm)}
 
 
-def make_inputs(cfg, rows, device, seed=7, bias2_seed=None):
-    """Synthetic OpenFold-shaped inputs: U[-1,1) rounded once to the
-    compute dtype; mask bias1 in {0,-1e9} at 10% (key 0 never masked). The pair
-    bias is drawn from `bias2_seed` when given (identical on every rank)."""
-    import torch
+def make_inputs(cfg, rows, pin=False):
+    """Synthetic OpenFold-shaped inputs, drawn exactly like the reference's instance generator
+    (SeededRng / derived_rng / random_uniform, run.cpp:178-195 — ported in
+    paper_2310_04610_b200/inputs.py and pinned bit-for-bit to oracle/_ref): U[-1,1) rounded once to
+    the compute dtype, Q, K, V, pair bias from stream 0, dO from stream 2^20, the DS4Sci mask bias1 in
+    {0, -1e9} at 10 % from stream 2^21 (key 0 never masked). `rows` = (lo, hi) of the config's rows:
+    every rank, the GPU arm and the reference arm draw the same values for the same rows. Host
+    tensors."""
+    from paper_2310_04610_b200.inputs import random_problem
 
     Bo, Nr, L, H, D, dt, _ = cfg
-    dtype = {"f32": torch.float32, "bf16": torch.bfloat16}[dt]
-    g = torch.Generator(device=device).manual_seed(seed)
-    lo, hi = rows
-    u = lambda *s: (torch.rand(*s, generator=g, device=device) * 2 - 1)
-    # generate the full tensors' row range deterministically (same values on every rank)
-    full = lambda: u(Bo, Nr, L, H, D)
-    q, k, v, do = full(), full(), full(), full()
-    m = torch.rand(Bo, Nr, 1, 1, L, generator=g, device=device) < 0.1
-    m[..., 0] = False
-    b1 = torch.where(m, -1e9, 0.0)
-    if bias2_seed is not None:
-        g.manual_seed(bias2_seed + 1)
-    b2 = u(Bo, 1, H, L, L)
-    sl = lambda t: t[:, lo:hi].contiguous()
-    out = [sl(q), sl(k), sl(v), sl(do), sl(b1), b2]
-    del q, k, v, do
-    return [t.to(dtype) for t in out]
+    return list(random_problem(Bo, Nr, L, H, D, dtype=dt, seed=7, rows=rows, pin=pin))
 
 
-def cpu_baseline(cfg, sample_rows, threads):
-    """Reference attn_forward_tiled + attn_backward_tiled (oracle/_ref, the
-    reference's own sources) in F32 on `sample_rows` rows, row-sharded over
-    `threads` host threads. Falls back to the C restatement if _ref is absent."""
+def algorithmic(B, L, H, D, elem=2):
+    """Per-call algorithmic FLOP and bytes (SURVEY §8(d) conventions) of the forward and backward."""
+    n = B * L * H * D
+    fwd = {"flop": 4.0 * B * H * L * L * D,
+           "bytes": 4 * elem * n + 4 * B * H * L + elem * H * L * L + elem * B * L}  # Q K V in, O + LSE out
+    bwd = {"flop": 10.0 * B * H * L * L * D,  # Q K V O dO in, dQ dK dV out, LSE in, bias2 in, dBias2 fp32 out
+           "bytes": 8 * elem * n + 4 * B * H * L + elem * H * L * L + 4 * H * L * L + elem * B * L}
+    return fwd, bwd
+
+
+def cpu_baseline(cfg, sample_rows, threads, inputs=None):
+    """Reference attn_forward_tiled + attn_backward_tiled (oracle/_ref, the reference's own
+    sources) in F32 on the first `sample_rows` rows of the config's inputs (the same values the GPU
+    arm computes on), row-sharded over `threads` host threads. Falls back to the C restatement if
+    _ref is absent."""
     import numpy as np
-    import torch
 
     from oracle import oracle as O
 
     Bo, Nr, L, H, D, dt, _ = cfg
-    q, k, v, do, b1, b2 = make_inputs(cfg, (0, sample_rows), "cpu")
-    f = lambda t: t.float().numpy().reshape(-1, L, H, D) if t.dim() == 5 and t.shape[-1] == D else t.float().numpy()
+    q, k, v, do, b1, b2 = inputs if inputs is not None else make_inputs(cfg, (0, sample_rows))
+    f = lambda t: t[0, :sample_rows].float().numpy().reshape(-1, L, H, D)
     qn, kn, vn, don = (f(t) for t in (q, k, v, do))
-    b2n = b2.float().numpy().reshape(H, L, L)
+    b2n = b2[0, 0].float().numpy()
     t0 = time.perf_counter()
     if O.ref_available():
         O.ref_threaded_f32(qn, kn, vn, b2n, don, threads)
         kind = "reference"
     else:
         p = O.Problem(sample_rows, L, H, D)
-        O.fwd_bwd_threaded(p, threads, qn, kn, vn, don, b1.float().numpy().reshape(-1, L), b2n)
+        O.fwd_bwd_threaded(p, threads, qn, kn, vn, don, b1[0, :sample_rows].float().numpy().reshape(-1, L), b2n)
         kind = "port"
     dt_s = time.perf_counter() - t0
     tf = flops(sample_rows, L, H, D) / dt_s / 1e12
     return {"value": tf, "unit": UNIT, "cores": threads, "kind": kind,
-            "sample": f"{sample_rows} of {Bo * Nr} rows of {cfg[6]}, F32 tiled fwd+bwd (tile 64,64,1), "
-                      f"{dt_s:.2f} s; mask bias omitted (the reference has no bias1)" if kind == "reference"
-                      else f"{sample_rows} rows, oracle port, {dt_s:.2f} s"}
+            "sample": f"rows 0..{sample_rows - 1} of {Bo * Nr} of {cfg[6]} (the GPU arm's input values), "
+                      f"F32 tiled fwd+bwd (tile 64,64,1), {dt_s:.2f} s; mask bias omitted (the reference has no "
+                      f"bias1)" if kind == "reference" else f"{sample_rows} rows, oracle port, {dt_s:.2f} s"}
+
+
+def parity_block(cfg, host, outs, rows, threads):
+    """Row sample of this run's own outputs against the oracle (the F32 restatement of
+    attention_tiled.cpp:57-340 with the mask term) on the same input values; dBias2 on the reduced
+    problem of the sampled rows, computed identically on both sides. Normalized max-abs error
+     with the reference-style floored max relative error beside it."""
+    import numpy as np
+
+    from oracle import oracle as O
+
+    Bo, Nr, L, H, D, dt, _ = cfg
+    q, k, v, do, b1, b2 = host
+    f = lambda t: np.ascontiguousarray(t[0, rows].float().numpy(), dtype=np.float64)
+    p = O.Problem(len(rows), L, H, D, fmt=O.F32)
+    wo, wl, wdq, wdk, wdv, wdb2 = O.fwd_bwd_threaded(
+        p, threads, f(q).reshape(-1, L, H, D), f(k).reshape(-1, L, H, D), f(v).reshape(-1, L, H, D),
+        f(do).reshape(-1, L, H, D), f(b1).reshape(-1, L), b2[0, 0].double().numpy())
+    want = {"O": wo, "LSE": wl.transpose(1, 0, 2), "dQ": wdq, "dK": wdk, "dV": wdv, "dBias2(sample rows)": wdb2}
+
+    def err(g, w):
+        g, w = np.asarray(g, np.float64), np.asarray(w, np.float64)
+        nmax = float(np.abs(g - w).max() / max(np.abs(w).max(), 1e-30))
+        den = np.maximum(np.maximum(np.abs(g), np.abs(w)), max(1e-3 * np.abs(w).max(), 1e-8))
+        return {"nmax": nmax, "ref_rel": float((np.abs(g - w) / den).max())}
+
+    res = {n: err(outs[n], want[n]) for n in want}
+    tol = 1e-2 if dt != "f32" else 1e-4
+    return {"rows": rows, "metric": "normalized max-abs error vs the oracle on identical inputs",
+            "tol": tol, "pass": all(r["nmax"] <= tol for r in res.values()), "errors": res}
 
 
 def run_reference_arm(args, cfg):
@@ -185,24 +213,25 @@ def run_reference_arm(args, cfg):
         return
     threads = os.cpu_count() or 1
     Bo, Nr, L, H, D, dt, desc = cfg
-    # bounded sample per step: one row per host thread, shrunk so that the
-    # whole (warmup + steps) run stays within ~4 minutes
+    # bounded sample per step: one row per host thread, shrunk so that the whole (warmup + steps)
+    # run stays within ~4 minutes; the rows' values are the GPU arm's (same generator, same streams)
     sample = min(Bo * Nr, threads)
-    first = cpu_baseline(cfg, sample, threads)
+    host = make_inputs(cfg, (0, sample))
+    first = cpu_baseline(cfg, sample, threads, host)
     per_step = flops(sample, L, H, D) / (first["value"] * 1e12)
     budget = 240.0 / max(1, args.steps + args.warmup)
     if per_step > budget:
         sample = max(1, int(sample * budget / per_step))
         threads = min(threads, sample)
     for _ in range(args.warmup - 1):
-        cpu_baseline(cfg, sample, threads)
-    vals = [cpu_baseline(cfg, sample, threads) for _ in range(args.steps)]
+        cpu_baseline(cfg, sample, threads, host)
+    vals = [cpu_baseline(cfg, sample, threads, host) for _ in range(args.steps)]
     v = statistics.median(x["value"] for x in vals)
     ms = flops(sample, L, H, D) / (v * 1e12) * 1e3
     line = {"metric": METRIC, "value": v, "unit": UNIT, "n_gpus": 0, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": args.scaling,
-            "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-            "config": {"workload": desc, "Bo": Bo, "N": Nr, "L": L, "H": H, "D": D,
+            "vs_baseline": None, "dtype": "f32", "data": "synthetic (reference SeededRng streams)",
+            "config": {"workload": desc, "config": args.config, "Bo": Bo, "N": Nr, "L": L, "H": H, "D": D,
                        "parallelism": f"cpu_threads{threads}"},
             "impl": "reference",
             "cpu_baseline": {"value": v, "unit": UNIT, "cores": threads, "kind": vals[0]["kind"],
@@ -226,11 +255,13 @@ def main():
     ap.add_argument("--config", default="c4", choices=sorted(CONFIGS))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-parity", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=20,
                     help="end-to-end steps timed (pipeline fill and drain amortised over them)")
     ap.add_argument("--all-configs", action="store_true", help="also time c1..c5 and attach them")
-    ap.add_argument("--scaling", default="weak", choices=["weak", "strong"],
-                    help="weak: each rank owns a full config's rows; strong: the config's rows split over ranks")
+    ap.add_argument("--scaling", default="strong", choices=["weak", "strong"],
+                    help="strong: the config's rows split over ranks (headline); weak: each rank owns a "
+                         "full config's rows")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     # stdout carries exactly one JSON line: anything else written to fd 1 (library banners such as
@@ -257,16 +288,20 @@ def main():
     dev = torch.device("cuda", local)
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)
+    # Timed loops run asynchronously: the NumericError host round trip (a stream sync per call) is
+    # off there; the checked mode is timed separately below and reported beside the headline.
+    E.set_numeric_checks(False)
 
     Bo, Nr, L, H, D, dt, desc = cfg
-    if args.scaling == "weak":  # rank r owns rows [r*Nr, (r+1)*Nr) of an N*Nr-row problem
-        q, k, v, do, b1, b2 = (t.to(dev) for t in make_inputs(cfg, (0, Nr), dev, seed=7 + 1000 * rank,
-                                                               bias2_seed=7))
-        B_local, B_total = Bo * Nr, Bo * Nr * world
-    else:
-        lo, hi = shard_rows(Nr, world, rank)
-        q, k, v, do, b1, b2 = (t.to(dev) for t in make_inputs(cfg, (lo, hi), dev))
-        B_local, B_total = Bo * (hi - lo), Bo * Nr
+
+    def rows_of(r, n):
+        return shard_rows(Nr, n, r) if args.scaling == "strong" else (0, Nr)
+
+    lo, hi = rows_of(rank, world)
+    host = make_inputs(cfg, (lo, hi), pin=True)
+    q, k, v, do, b1, b2 = (t.to(dev) for t in host)
+    B_local = Bo * (hi - lo)
+    B_total = Bo * Nr if args.scaling == "strong" else Bo * Nr * world
 
     def step():
         return sharded_fwd_bwd(q, k, v, do, b1, b2)
@@ -285,20 +320,20 @@ def main():
     E.evoformer_attention_backward(do, q, k, v, o, lse, b1, b2, need_dbias1=False)
     n_bwd = E.last_launch_count()
     path = E.resolved_path(q, b1, b2)
+    bwd_path = E.resolved_path(q, b1, b2, direction="bwd")
 
     # ---- peak memory of one fwd+bwd beyond the I/O tensors
     torch.cuda.synchronize()
-    io = [q, k, v, do, b1, b2]
     base = torch.cuda.memory_allocated()
     torch.cuda.reset_peak_memory_stats()
     r = step()
     torch.cuda.synchronize()
-    outs = sum(t.numel() * t.element_size() for t in (r.o, r.dq, r.dk, r.dv) if t is not None)
+    outs = sum(t.numel() * t.element_size() for t in (r.o, r.lse, r.dq, r.dk, r.dv) if t is not None)
     outs += sum(t.numel() * t.element_size() for t in (r.dbias1, r.dbias2) if t is not None)
     peak_extra = torch.cuda.max_memory_allocated() - base - outs
     del r
 
-    # ---- timed region: K steps, barrier + sync on both sides, CUDA events
+    # ---- timed region: K steps, barrier + sync on both sides, CUDA events on the launching stream
     stream = torch.cuda.current_stream()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(local) as clk:
@@ -318,7 +353,6 @@ def main():
     total_flops = flops(B_total, L, H, D)
     value = total_flops / (ms * 1e-3) / 1e12
 
-    # ---- per-kernel timing (forward call, backward call) on the launching stream
     def time_call(fn, n):
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         torch.cuda.synchronize()
@@ -329,37 +363,54 @@ def main():
         torch.cuda.synchronize()
         return a.elapsed_time(b) / n
 
+    # the same step with the reference's NumericError checks on (each call waits for its stream)
+    E.set_numeric_checks(True)
+    barrier()
+    ms_checked = time_call(step, max(5, args.steps // 4))
+    E.set_numeric_checks(False)
+
+    # ---- per-call timing (forward call, backward call) on the launching stream; the dominant call's
+    # roofline against the bound of the SURVEY §8(d) model (max of the FLOP and byte times)
     o, lse = E.evoformer_attention_forward(q, k, v, b1, b2)
     nk = max(10, args.steps // 2)
     fwd_ms = time_call(lambda: E.evoformer_attention_forward(q, k, v, b1, b2), nk)
     bwd_ms = time_call(lambda: E.evoformer_attention_backward(do, q, k, v, o, lse, b1, b2,
                                                               need_dbias1=False), nk)
     pk = peaks()
-    f_fwd = 4.0 * B_local * H * L * L * D
-    f_bwd = 10.0 * B_local * H * L * L * D
-    dom = ("bwd", f_bwd, bwd_ms) if bwd_ms >= fwd_ms else ("fwd", f_fwd, fwd_ms)
-    achieved = dom[1] / (dom[2] * 1e-3) / 1e12
+    elem = 4 if dt == "f32" else 2
+    a_fwd, a_bwd = algorithmic(B_local, L, H, D, elem)
+    dom_name, dom, dom_ms = ("bwd", a_bwd, bwd_ms) if bwd_ms >= fwd_ms else ("fwd", a_fwd, fwd_ms)
+    t_flop = dom["flop"] / (pk["bf16_tflops"] * 1e12)
+    t_hbm = dom["bytes"] / (pk["hbm_gbs"] * 1e9)
+    bound = "hbm" if t_hbm >= t_flop else "tensor"
+    achieved = dom["bytes"] / (dom_ms * 1e-3) / 1e9 if bound == "hbm" else dom["flop"] / (dom_ms * 1e-3) / 1e12
+    peak = pk["hbm_gbs"] if bound == "hbm" else pk["bf16_tflops"]
     traffic = None
     try:
         with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
-            tr = json.load(f).get(f"{args.config}_{dom[0]}_{path}")
-            traffic = tr
+            traffic = json.load(f).get(f"{args.config}_{dom_name}_{path}")
     except Exception:
         pass
-    roofline = {"bound": "tensor", "achieved": achieved, "peak": pk["bf16_tflops"], "unit": "TFLOP/s",
-                "frac": achieved / pk["bf16_tflops"], "traffic": traffic, "kernel": f"{dom[0]} ({path})",
+    roofline = {"bound": bound, "achieved": achieved, "peak": peak, "unit": "GB/s" if bound == "hbm" else "TFLOP/s",
+                "frac": achieved / peak, "traffic": traffic, "kernel": f"{dom_name} call ({path})",
                 "peak_source": pk["source"],
-                "kernels": {"fwd": {"ms": fwd_ms, "tflops": f_fwd / fwd_ms / 1e9},
-                            "bwd": {"ms": bwd_ms, "tflops": f_bwd / bwd_ms / 1e9}},
-                "step_roofline_frac": (max(total_flops / world / (pk["bf16_tflops"] * 1e12),
-                                           ideal_bytes(B_local, L, H, D) / (pk["hbm_gbs"] * 1e9))
+                "algorithmic": {"flop": dom["flop"], "bytes": dom["bytes"], "t_flop_us": t_flop * 1e6,
+                                "t_hbm_us": t_hbm * 1e6},
+                "tensor_frac": dom["flop"] / (dom_ms * 1e-3) / 1e12 / pk["bf16_tflops"],
+                "hbm_frac": dom["bytes"] / (dom_ms * 1e-3) / 1e9 / pk["hbm_gbs"],
+                "kernels": {"fwd": {"ms": fwd_ms, "tflops": a_fwd["flop"] / fwd_ms / 1e9,
+                                    "gbs": a_fwd["bytes"] / fwd_ms / 1e6},
+                            "bwd": {"ms": bwd_ms, "tflops": a_bwd["flop"] / bwd_ms / 1e9,
+                                    "gbs": a_bwd["bytes"] / bwd_ms / 1e6}},
+                "step_roofline_frac": (max(flops(B_local, L, H, D) / (pk["bf16_tflops"] * 1e12),
+                                           ideal_bytes(B_local, L, H, D, elem) / (pk["hbm_gbs"] * 1e9))
                                        / (ms * 1e-3))}
 
     # ---- end to end through the public API with pinned host buffers. Every step copies its inputs
     # host->device and its gradients device->host; the copies of neighbouring steps overlap the
     # compute on separate streams (inputs double-buffered), which is how a training loop feeds it.
-    host_in = [t.cpu().pin_memory() for t in (q, k, v, do, b1, b2)]
-    dev_sets = [[torch.empty_like(t) for t in (q, k, v, do, b1, b2)] for _ in range(2)]
+    host_in = host
+    dev_sets = [[torch.empty_like(t, device=dev) for t in host_in] for _ in range(2)]
     r = step()
     host_out = [torch.empty(t.shape, dtype=t.dtype, pin_memory=True) for t in (r.dq, r.dk, r.dv, r.dbias2)]
     h2d = sum(t.numel() * t.element_size() for t in host_in)
@@ -417,7 +468,7 @@ def main():
         for name, c in CONFIGS.items():
             if name == args.config:
                 continue
-            qq, kk, vv, dd, bb1, bb2 = (x.to(dev) for x in make_inputs(c, (0, c[1]), dev))
+            qq, kk, vv, dd, bb1, bb2 = (x.to(dev) for x in make_inputs(c, (0, c[1])))
             for _ in range(3):
                 sharded_fwd_bwd(qq, kk, vv, dd, bb1, bb2)
             n = 20 if name != "c5" else 3
@@ -443,31 +494,62 @@ def main():
         del tq, tk, tv, tb, tdo, tm
         torch.cuda.empty_cache()
 
+    th = os.cpu_count() or 1
+    parity = None
+    if rank == 0 and not args.no_parity:
+        # this run's own outputs on a row sample of rank 0's shard, against the oracle on the same values
+        try:
+            nloc = hi - lo
+            rows = sorted(set(int(round(x)) for x in [0, nloc // 3, (2 * nloc) // 3, nloc - 1]))
+            if args.config == "c5":
+                rows = [0, nloc - 1]
+            res = sharded_fwd_bwd(q, k, v, do, b1, b2)
+            idx = torch.tensor(rows, device=dev)
+            sel = lambda x: x[0].index_select(0, idx).float().cpu().numpy()
+            outs = {"O": sel(res.o), "LSE": res.lse.index_select(0, idx).cpu().numpy(), "dQ": sel(res.dq),
+                    "dK": sel(res.dk), "dV": sel(res.dv)}
+            sub = lambda x: x[:, idx].contiguous()
+            if world > 1:  # the reduced problem of the sampled rows, on this rank alone
+                from paper_2310_04610_b200.evoformer_attention import (evoformer_attention_backward,
+                                                                       evoformer_attention_forward)
+                so, sl = evoformer_attention_forward(sub(q), sub(k), sub(v), sub(b1), b2)
+                sdb2 = evoformer_attention_backward(sub(do), sub(q), sub(k), sub(v), so, sl, sub(b1), b2)[4]
+            else:
+                sdb2 = sharded_fwd_bwd(sub(q), sub(k), sub(v), sub(do), sub(b1), b2).dbias2
+            outs["dBias2(sample rows)"] = sdb2[0, 0].cpu().numpy()
+            parity = parity_block(cfg, host, outs, rows, th)
+            parity["rows"] = [lo + x for x in rows]
+        except Exception as e:  # reported, never hidden
+            parity = {"pass": False, "error": repr(e)}
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
-            th = os.cpu_count() or 1
-            cpu = cpu_baseline(cfg, max(th, (Bo * Nr) // 64) if args.config != "c5" else 2, th)
+            sample = max(th, (Bo * Nr) // 64) if args.config != "c5" else 2
+            cpu = cpu_baseline(cfg, min(sample, hi - lo), th, host)
         except Exception as e:  # reported, never silently substituted
             cpu = {"value": None, "unit": UNIT, "cores": 0, "kind": "unavailable", "sample": repr(e)}
 
     if rank == 0:
-        naive = 3 * H * B_local * L * L * (2 if dt == "bf16" else 4)
+        naive = 3 * H * B_local * L * L * elem
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": args.scaling,
-            "vs_baseline": None, "dtype": dt, "data": "synthetic",
+            "vs_baseline": None, "dtype": dt, "data": "synthetic (reference SeededRng streams, seed 7)",
             "config": {"workload": desc, "config": args.config, "Bo": Bo, "N": Nr, "L": L, "H": H,
                        "D": D, "biases": "mask bias1 [Bo,N,1,1,L] + pair bias2 [Bo,1,H,L,L]",
                        "rows_per_rank": B_local, "rows_total": B_total,
-                       "parallelism": f"rows_sharded_dp{world}", "kernel_path": path,
-                       "l2": "inputs+outputs larger than L2 (no flush needed)" if ideal_bytes(B_local, L, H, D) > 126e6
-                       else "working set smaller than L2 (not flushed)"},
+                       "parallelism": f"rows_sharded_dp{world}", "kernel_path": path, "bwd_kernel_path": bwd_path,
+                       "numeric_checks": "off in the timed loop (ms_per_step_checked: on)",
+                       "l2": "inputs+outputs larger than L2 (no flush needed)"
+                       if ideal_bytes(B_local, L, H, D, elem) > 126e6 else "working set smaller than L2 (not flushed)"},
+            "ms_per_step_checked": ms_checked,
             "peak_mem": {"extra_bytes_per_rank": int(peak_extra), "naive_logits_bytes": naive,
                          "o_l_plan_bytes": 8 * B_local * H * L + 4 * H * L * L,
                          # the reference attn-bench column (run.cpp:223-234): naive / tiled peak
                          "reduction_ratio": naive / max(int(peak_extra), 1)},
             "roofline": roofline,
+            "parity": parity,
             "cpu_baseline": cpu,
             "e2e": {"value": total_flops / (e2e_ms * 1e-3) / 1e12, "unit": UNIT, "ms_per_step": e2e_ms,
                     "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},

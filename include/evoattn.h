@@ -81,6 +81,17 @@ typedef struct {
                              through the strides, no transposed copy. Requires Bo == 1; bias1, bias2,
                              lse and the dbias outputs stay canonical ([N, L], [H, L, L], [N, H, L]).
                              0 = canonical [Bo, N, L, H, D]. */
+  int check_numerics;     /* 1 = NumericError contract of the reference (attention_tiled.cpp:49-65,
+                             125-127, 209): the kernels flag NaN inputs (Q, K, V, biases, dO) and
+                             non-finite logit rows (a NaN / non-finite LSE or delta, NaN outputs);
+                             the call then synchronises its stream and returns EVO_ERR_NUMERIC.
+                             Logits of -inf at some keys (masking) are allowed; a row with no finite
+                             logit is flagged. 0 = no checks, fully asynchronous. */
+  int deterministic;      /* backward: AccumPolicy::deterministic (attention_tiled.hpp:35-44; the
+                             reference default): every cross-CTA reduction (dBias2, dBias1, dQ and
+                             the chunked dK/dV) runs in a fixed order, so two runs are bit-identical
+                             (SPEC.md:211). The SIMT backward is always ordered. 0 = unordered fp32
+                             reductions (faster). */
 } evo_attn_desc;
 
 size_t evo_attn_fwd_workspace_size(const evo_attn_desc* desc);
@@ -106,6 +117,11 @@ evo_status evo_attn_bwd(const evo_attn_desc* desc, const void* dout, const void*
 /* Which kernel family AUTO resolves to for this descriptor (EVO_PATH_SIMT or
  * EVO_PATH_TCGEN05); negative if the descriptor is invalid. */
 int evo_attn_resolved_path(const evo_attn_desc* desc);
+
+/* Which kernel family the BACKWARD resolves to (the tcgen05 backward's envelope is narrower than
+ * the forward's: 16-bit, D in {16, 32}, L % 8 == 0); negative if invalid or an explicit
+ * EVO_PATH_TCGEN05 request cannot be honoured. */
+int evo_attn_resolved_bwd_path(const evo_attn_desc* desc);
 
 /* Number of kernel launches the last fwd / bwd call issued on this thread. */
 int evo_attn_last_launch_count(void);

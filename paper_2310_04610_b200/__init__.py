@@ -9,7 +9,7 @@ from ._native import (CudaError, EvoAttnError, NumericError, UnsupportedError, U
                       ValidationError)
 from .evoformer_attention import (DS4Sci_EvoformerAttention, EvoformerAttentionFunction,
                                   evoformer_attention_backward, evoformer_attention_forward,
-                                  last_launch_count, resolved_path)
+                                  last_launch_count, numeric_checks, resolved_path, set_numeric_checks)
 from .variants import (AttentionVariant, chunked_forward, layout_from_msa, variant_attention, variant_forward,
                        variant_from_name)
 
@@ -18,5 +18,5 @@ __all__ = [
     "evoformer_attention_backward", "last_launch_count", "resolved_path", "EvoAttnError",
     "ValidationError", "NumericError", "UsageError", "CudaError", "UnsupportedError",
     "AttentionVariant", "variant_attention", "variant_from_name", "layout_from_msa",
-    "chunked_forward", "variant_forward",
+    "chunked_forward", "variant_forward", "set_numeric_checks", "numeric_checks",
 ]

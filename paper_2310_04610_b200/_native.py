@@ -17,7 +17,7 @@ EVO_PATH_AUTO, EVO_PATH_SIMT, EVO_PATH_TCGEN05 = 0, 1, 2
 # Symbols declared in include/evoattn.h (checked by tests/test_capi.py).
 EXPORTED = (
     "evo_attn_fwd_workspace_size", "evo_attn_bwd_workspace_size", "evo_attn_fwd", "evo_attn_bwd",
-    "evo_attn_resolved_path", "evo_attn_last_launch_count", "evo_attn_last_error",
+    "evo_attn_resolved_path", "evo_attn_resolved_bwd_path", "evo_attn_last_launch_count", "evo_attn_last_error",
     "evo_attn_version", "evo_random_uniform", "evo_random_mask",
 )
 
@@ -27,7 +27,7 @@ class Desc(C.Structure):
                 ("D", C.c_int64), ("dtype", C.c_int), ("scale", C.c_double),
                 ("has_bias1", C.c_int), ("has_bias2", C.c_int), ("dbias_dtype", C.c_int),
                 ("path", C.c_int), ("dbias2_multicast", C.c_void_p), ("need_dbias1", C.c_int),
-                ("axes_swapped", C.c_int)]
+                ("axes_swapped", C.c_int), ("check_numerics", C.c_int), ("deterministic", C.c_int)]
 
 
 _lib = None
@@ -59,9 +59,15 @@ def load(build_if_missing: bool = True):
     lib.evo_attn_bwd.restype = C.c_int
     lib.evo_attn_resolved_path.argtypes = [dp]
     lib.evo_attn_resolved_path.restype = C.c_int
+    if hasattr(lib, "evo_attn_resolved_bwd_path"):
+        lib.evo_attn_resolved_bwd_path.argtypes = [dp]
+        lib.evo_attn_resolved_bwd_path.restype = C.c_int
     lib.evo_attn_last_launch_count.restype = C.c_int
     lib.evo_attn_last_error.restype = C.c_char_p
     lib.evo_attn_version.restype = C.c_char_p
+    if not hasattr(lib, "evo_random_uniform"):  # an older A/B variant (tools/ab_time.py)
+        _lib = lib
+        return lib
     lib.evo_random_uniform.argtypes = [C.c_uint64, C.c_uint64, C.c_int64, C.c_int64, C.c_double, C.c_double,
                                        C.c_int, vp]
     lib.evo_random_uniform.restype = C.c_int

@@ -52,6 +52,17 @@ __device__ __forceinline__ float2 ex2_poly2(float2 x) {
                      __int_as_float(__float_as_int(p.y) + (ny << 23)));
 }
 
+// acc[x] += part[0][x] + part[1][x] + ... + part[np-1][x], added one part at a time in ascending order
+// (fp32): the fixed-order reduction of row / head / chunk partials — bit-reproducible.
+template <typename F>
+__global__ void ordered_sum_kernel(const F* __restrict__ part, int np, size_t stride, F* __restrict__ acc, size_t n) {
+  for (size_t x = blockIdx.x * (size_t)blockDim.x + threadIdx.x; x < n; x += (size_t)gridDim.x * blockDim.x) {
+    F a = acc[x];
+    for (int k = 0; k < np; ++k) a += part[(size_t)k * stride + x];
+    acc[x] = a;
+  }
+}
+
 // Shape/stride bundle shared by every kernel. Canonical row index b in
 // [0, B) with B = Bo*N; tensors are (B, L, H, D) row-major.
 struct Shape {
@@ -61,7 +72,15 @@ struct Shape {
   const void* bias1;  // (B, L) or null
   const void* bias2;  // (Bo, H, L, L) or null
   int swapped;        // 1: q/k/v/o are (L, B, H, D) — the raw msa_col / tri_end layout (Bo == 1)
+  int* flag;          // numeric-check word (NaN / non-finite results set it), or null: no checks
 };
+
+// NumericError detection (attention_tiled.cpp:49-53, 62-65, 125-127, 209): a NaN input or a
+// non-finite logit row shows up as a non-finite LSE / delta or a NaN output; the kernels OR a flag
+// the C-ABI reads back when the caller asked for numeric checks.
+__device__ __forceinline__ void flag_if(int* flag, bool bad) {
+  if (flag && bad) atomicOr(flag, 1);
+}
 
 __device__ __forceinline__ size_t row_off(const Shape& s, int b, int i, int h) {
   return ((s.swapped ? (size_t)i * s.B + b : (size_t)b * s.L + i) * s.H + h) * (size_t)s.D;

@@ -4,6 +4,7 @@
 // Validation mirrors AttentionProblem::validate (attention.cpp:49-86) and
 // attn_backward_tiled's stats checks (attention_tiled.cpp:196-209), mapped to
 // evo_status codes instead of exceptions (errors.hpp:15-30).
+#include <algorithm>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
@@ -43,8 +44,15 @@ evo_status validate(const evo_attn_desc* d) {
   return EVO_OK;
 }
 
+// The tcgen05 kernels carry 1/scale in 16-bit UMMA operands (the bias augmentation steps): it must be
+// a finite normal number of the problem's 16-bit format; other scales take the SIMT kernels.
+bool scale_fits_16bit(const evo_attn_desc* d) {
+  const double c = std::fabs(1.0 / d->scale);
+  return d->dtype == EVO_F16 ? (c >= 6.103515625e-05 && c <= 65504.0) : (c >= 1.1754943508222875e-38 && c <= 3.3e38);
+}
+
 bool tc_eligible(const evo_attn_desc* d) {
-  return d->dtype != EVO_F32 && (d->D == 16 || d->D == 32 || d->D == 64) &&
+  return d->dtype != EVO_F32 && (d->D == 16 || d->D == 32 || d->D == 64) && scale_fits_16bit(d) &&
          evo::tc::device_supported();
 }
 
@@ -54,7 +62,7 @@ int resolve(const evo_attn_desc* d) {
   return tc_eligible(d) ? EVO_PATH_TCGEN05 : EVO_PATH_SIMT;
 }
 
-evo::Shape make_shape(const evo_attn_desc* d, const void* b1, const void* b2) {
+evo::Shape make_shape(const evo_attn_desc* d, const void* b1, const void* b2, int* flag = nullptr) {
   evo::Shape s;
   s.B = (int)(d->Bo * d->N);
   s.N = (int)d->N;
@@ -66,26 +74,56 @@ evo::Shape make_shape(const evo_attn_desc* d, const void* b1, const void* b2) {
   s.bias1 = b1;
   s.bias2 = b2;
   s.swapped = d->axes_swapped;
+  s.flag = d->check_numerics ? flag : nullptr;
   return s;
 }
 
-// Bwd workspace layout: [delta B*H*L f32][dbias2 acc Bo*H*L*L f32][dbias1 acc B*L f32][tc scratch]
+// Every workspace starts with a 256-byte header: word 0 is the numeric-check flag.
+constexpr size_t kHeader = 256;
+
+// SIMT backward: dBias2 / dBias1 partial planes of one row batch (ordered, atomic-free reduction);
+// batches stay inside one outer batch and are sized so the dBias2 planes fit kSimtPartCap.
+constexpr size_t kSimtPartCap = (size_t)512 << 20;
+int64_t simt_batch_rows(const evo_attn_desc* d) {
+  if (!d->has_bias2) return d->N;
+  const size_t plane = (size_t)d->H * d->L * d->L * 4;
+  return std::max<int64_t>(1, std::min<int64_t>(d->N, (int64_t)(kSimtPartCap / plane)));
+}
+
+// Bwd workspace layout: [header][delta B*H*L f32][dbias2 acc Bo*H*L*L f32][dbias1 acc B*L f32]
+// [SIMT partial planes of one row batch][tc scratch]
 struct BwdWs {
-  size_t delta, db2, db1, tc, total;
+  size_t delta, db2, db1, db2p, db1p, tc, total;
 };
+
+// Workspace sizing follows the kernels the call will run on the target device (sm_100a); on a host
+// without one (sizing only) the tcgen05 envelope is assumed.
+bool simt_bwd_path(const evo_attn_desc* d) {
+  if (d->path == EVO_PATH_SIMT) return true;
+  const bool tc = d->dtype != EVO_F32 && (d->D == 16 || d->D == 32) && d->L % 8 == 0 && scale_fits_16bit(d);
+  return !tc;
+}
 
 BwdWs bwd_layout(const evo_attn_desc* d) {
   BwdWs w{};
   const size_t B = (size_t)(d->Bo * d->N);
-  size_t off = 0;
+  size_t off = kHeader;
   w.delta = off;
   off += align_up(B * d->H * d->L * 4);
   w.db2 = off;
   if (d->has_bias2) off += align_up((size_t)d->Bo * d->H * d->L * d->L * 4);
   w.db1 = off;
   if (d->has_bias1 && d->need_dbias1) off += align_up(B * d->L * 4);
-  w.tc = off;
-  off += align_up(evo::tc::bwd_scratch_bytes(d));
+  w.db2p = w.db1p = w.tc = off;
+  if (simt_bwd_path(d)) {
+    const size_t nb = (size_t)simt_batch_rows(d);
+    if (d->has_bias2) off += align_up(nb * d->H * d->L * d->L * 4);
+    w.db1p = off;
+    if (d->has_bias1 && d->need_dbias1) off += align_up((size_t)d->H * nb * d->L * 4);
+    w.tc = off;
+  } else {
+    off += align_up(evo::tc::bwd_scratch_bytes(d));
+  }
   w.total = off;
   return w;
 }
@@ -110,27 +148,46 @@ evo_status simt_fwd_dispatch(const evo::Shape& s, const void* q, const void* k, 
   return EVO_OK;
 }
 
+void launch_ordered_sum(const float* part, int np, size_t stride, float* acc, size_t n, cudaStream_t st) {
+  const int blocks = (int)std::min<size_t>((n + 255) / 256, 148 * 16);
+  evo::ordered_sum_kernel<float><<<blocks, 256, 0, st>>>(part, np, stride, acc, n);
+  ++g_launches;
+}
+
+// SIMT backward over row batches inside each outer batch: dK/dV (+ the batch's dBias partial planes),
+// dQ, then the planes added in ascending order into the fp32 accumulators (no atomics: the result
+// is bit-reproducible, the reference's deterministic policy).
 template <typename T, int DP>
-void simt_bwd(const evo::Shape& s, const void* dout, const void* q, const void* k, const void* v,
-              const float* lse, const float* delta, void* dq, void* dk, void* dv, float* db1,
-              float* db2, cudaStream_t st) {
-  dim3 grid((s.L + evo::simt::Tiles<DP>::kRows - 1) / evo::simt::Tiles<DP>::kRows, s.H, s.B);
-  evo::simt::dkdv_kernel<T, DP><<<grid, evo::simt::Tiles<DP>::kRows, 0, st>>>(
-      s, (const T*)q, (const T*)k, (const T*)v, (const T*)dout, lse, delta, (T*)dk, (T*)dv, db1,
-      db2);
-  evo::simt::dq_kernel<T, DP><<<grid, evo::simt::Tiles<DP>::kRows, 0, st>>>(
-      s, (const T*)q, (const T*)k, (const T*)v, (const T*)dout, lse, delta, (T*)dq);
-  g_launches += 2;
+void simt_bwd(const evo_attn_desc* d, const evo::Shape& s, const void* dout, const void* q, const void* k,
+              const void* v, const float* lse, const float* delta, void* dq, void* dk, void* dv, float* db1,
+              float* db2, float* db1p, float* db2p, cudaStream_t st) {
+  const int64_t nb = simt_batch_rows(d);
+  const size_t plane = (size_t)s.H * s.L * s.L;
+  for (int ob = 0; ob < (int)d->Bo; ++ob)
+    for (int64_t n0 = 0; n0 < d->N; n0 += nb) {
+      const int rows = (int)std::min<int64_t>(nb, d->N - n0);
+      const int b0 = (int)(ob * d->N + n0);
+      dim3 grid((s.L + evo::simt::Tiles<DP>::kRows - 1) / evo::simt::Tiles<DP>::kRows, s.H, rows);
+      evo::simt::dkdv_kernel<T, DP><<<grid, evo::simt::Tiles<DP>::kRows, 0, st>>>(
+          s, (const T*)q, (const T*)k, (const T*)v, (const T*)dout, lse, delta, (T*)dk, (T*)dv, b0,
+          db1 ? db1p : nullptr, db2 ? db2p : nullptr);
+      evo::simt::dq_kernel<T, DP><<<grid, evo::simt::Tiles<DP>::kRows, 0, st>>>(
+          s, (const T*)q, (const T*)k, (const T*)v, (const T*)dout, lse, delta, (T*)dq, b0);
+      g_launches += 2;
+      if (db2) launch_ordered_sum(db2p, rows, plane, db2 + (size_t)ob * plane, plane, st);
+      if (db1) launch_ordered_sum(db1p, s.H, (size_t)rows * s.L, db1 + (size_t)b0 * s.L, (size_t)rows * s.L, st);
+    }
 }
 
 template <typename T>
-evo_status simt_bwd_dispatch(const evo::Shape& s, const void* dout, const void* q, const void* k,
-                             const void* v, const float* lse, const float* delta, void* dq,
-                             void* dk, void* dv, float* db1, float* db2, cudaStream_t st) {
-  if (s.D <= 8) simt_bwd<T, 8>(s, dout, q, k, v, lse, delta, dq, dk, dv, db1, db2, st);
-  else if (s.D <= 16) simt_bwd<T, 16>(s, dout, q, k, v, lse, delta, dq, dk, dv, db1, db2, st);
-  else if (s.D <= 32) simt_bwd<T, 32>(s, dout, q, k, v, lse, delta, dq, dk, dv, db1, db2, st);
-  else if (s.D <= 64) simt_bwd<T, 64>(s, dout, q, k, v, lse, delta, dq, dk, dv, db1, db2, st);
+evo_status simt_bwd_dispatch(const evo_attn_desc* d, const evo::Shape& s, const void* dout, const void* q,
+                             const void* k, const void* v, const float* lse, const float* delta, void* dq,
+                             void* dk, void* dv, float* db1, float* db2, float* db1p, float* db2p,
+                             cudaStream_t st) {
+  if (s.D <= 8) simt_bwd<T, 8>(d, s, dout, q, k, v, lse, delta, dq, dk, dv, db1, db2, db1p, db2p, st);
+  else if (s.D <= 16) simt_bwd<T, 16>(d, s, dout, q, k, v, lse, delta, dq, dk, dv, db1, db2, db1p, db2p, st);
+  else if (s.D <= 32) simt_bwd<T, 32>(d, s, dout, q, k, v, lse, delta, dq, dk, dv, db1, db2, db1p, db2p, st);
+  else if (s.D <= 64) simt_bwd<T, 64>(d, s, dout, q, k, v, lse, delta, dq, dk, dv, db1, db2, db1p, db2p, st);
   else return fail(EVO_ERR_UNSUPPORTED, "SIMT kernels support D <= 64");
   return EVO_OK;
 }
@@ -157,11 +214,30 @@ evo_status check_launch() {
   return EVO_OK;
 }
 
+// check_numerics: the kernels OR the header flag; the call waits for its stream and maps a raised
+// flag to NumericError (the reference throws from inside the operator: attention_tiled.cpp:49-65,
+// 125-127, 209).
+evo_status numeric_begin(const evo_attn_desc* d, int* flag, cudaStream_t st) {
+  if (d->check_numerics && cudaMemsetAsync(flag, 0, sizeof(int), st) != cudaSuccess)
+    return fail(EVO_ERR_CUDA, "numeric-check flag reset failed");
+  return EVO_OK;
+}
+evo_status numeric_end(const evo_attn_desc* d, const int* flag, cudaStream_t st, const char* what) {
+  evo_status e = check_launch();
+  if (e || !d->check_numerics) return e;
+  int h = 0;
+  if (cudaMemcpyAsync(&h, flag, sizeof(int), cudaMemcpyDeviceToHost, st) != cudaSuccess ||
+      cudaStreamSynchronize(st) != cudaSuccess)
+    return fail(EVO_ERR_CUDA, std::string("CUDA: ") + cudaGetErrorString(cudaGetLastError()));
+  if (h) return fail(EVO_ERR_NUMERIC, what);
+  return EVO_OK;
+}
+
 }  // namespace
 
 extern "C" {
 
-const char* evo_attn_version(void) { return "evoattn 0.1 sm_100a"; }
+const char* evo_attn_version(void) { return "evoattn 0.2 sm_100a"; }
 const char* evo_attn_last_error(void) { return g_err.c_str(); }
 int evo_attn_last_launch_count(void) { return g_launches; }
 
@@ -170,9 +246,17 @@ int evo_attn_resolved_path(const evo_attn_desc* d) {
   return resolve(d);
 }
 
+int evo_attn_resolved_bwd_path(const evo_attn_desc* d) {
+  if (validate(d) != EVO_OK) return -1;
+  const int p = resolve(d);
+  if (p < 0) return -1;
+  if (p == EVO_PATH_TCGEN05 && !evo::tc::bwd_available(d)) return d->path == EVO_PATH_TCGEN05 ? -1 : EVO_PATH_SIMT;
+  return p;
+}
+
 size_t evo_attn_fwd_workspace_size(const evo_attn_desc* d) {
   if (validate(d) != EVO_OK) return 0;
-  return evo::tc::fwd_scratch_bytes(d);
+  return kHeader + evo::tc::fwd_scratch_bytes(d);
 }
 
 size_t evo_attn_bwd_workspace_size(const evo_attn_desc* d) {
@@ -190,13 +274,15 @@ evo_status evo_attn_fwd(const evo_attn_desc* d, const void* q, const void* k, co
   if (!q || !k || !v || !o || !lse) return fail(EVO_ERR_VALIDATION, "q, k, v, o, lse must be non-null");
   if (d->has_bias1 != (bias1 != nullptr)) return fail(EVO_ERR_VALIDATION, "bias1 presence does not match the descriptor");
   if (d->has_bias2 != (bias2 != nullptr)) return fail(EVO_ERR_VALIDATION, "bias2 presence does not match the descriptor");
-  if (workspace_bytes < evo_attn_fwd_workspace_size(d)) return fail(EVO_ERR_VALIDATION, "workspace too small");
+  if (!workspace || workspace_bytes < evo_attn_fwd_workspace_size(d)) return fail(EVO_ERR_VALIDATION, "workspace too small");
   const int path = resolve(d);
-  if (path < 0) return fail(EVO_ERR_UNSUPPORTED, "tcgen05 path requested for an ineligible shape/dtype/device");
+  if (path < 0) return fail(EVO_ERR_UNSUPPORTED, "tcgen05 path requested for an ineligible shape/dtype/scale/device");
   cudaStream_t cs = (cudaStream_t)stream;
-  const evo::Shape s = make_shape(d, bias1, bias2);
+  int* flag = (int*)workspace;
+  if ((st = numeric_begin(d, flag, cs))) return st;
+  const evo::Shape s = make_shape(d, bias1, bias2, flag);
   if (path == EVO_PATH_TCGEN05) {
-    st = evo::tc::fwd(d, s, q, k, v, o, lse, workspace, cs, &g_launches, &g_err);
+    st = evo::tc::fwd(d, s, q, k, v, o, lse, (char*)workspace + kHeader, cs, &g_launches, &g_err);
     if (st) return st;
   } else {
     switch (d->dtype) {
@@ -206,7 +292,7 @@ evo_status evo_attn_fwd(const evo_attn_desc* d, const void* q, const void* k, co
     }
     if (st) return st;
   }
-  return check_launch();
+  return numeric_end(d, flag, cs, "attention logits are not finite or an input contains NaN (Q, K, V, bias)");
 }
 
 evo_status evo_attn_bwd(const evo_attn_desc* d, const void* dout, const void* q, const void* k,
@@ -231,13 +317,22 @@ evo_status evo_attn_bwd(const evo_attn_desc* d, const void* dout, const void* q,
   if (d->dbias2_multicast && (!dbias2 || d->dbias_dtype != EVO_F32 || !accumulate_dbias))
     return fail(EVO_ERR_VALIDATION,
                 "dbias2_multicast needs dbias2 (this rank's replica), dbias_dtype EVO_F32 and accumulate_dbias");
+  if (d->dbias2_multicast && d->deterministic)
+    return fail(EVO_ERR_VALIDATION, "dbias2_multicast reduces across GPUs in arrival order: not deterministic");
   const BwdWs w = bwd_layout(d);
   if (!workspace || workspace_bytes < w.total) return fail(EVO_ERR_VALIDATION, "workspace too small");
   const int path = resolve(d);
-  if (path < 0) return fail(EVO_ERR_UNSUPPORTED, "tcgen05 path requested for an ineligible shape/dtype/device");
+  if (path < 0) return fail(EVO_ERR_UNSUPPORTED, "tcgen05 path requested for an ineligible shape/dtype/scale/device");
+  const bool tc_bwd = path == EVO_PATH_TCGEN05 && evo::tc::bwd_available(d);
+  if (d->path == EVO_PATH_TCGEN05 && !tc_bwd)
+    return fail(EVO_ERR_UNSUPPORTED, "tcgen05 backward requested outside its envelope (16-bit, D 16/32, L % 8 == 0)");
+  if (d->dbias2_multicast && !tc_bwd)
+    return fail(EVO_ERR_UNSUPPORTED, "the multicast dBias2 reduction needs the tcgen05 backward (16-bit, D 16/32, L % 8 == 0)");
   cudaStream_t cs = (cudaStream_t)stream;
-  const evo::Shape s = make_shape(d, bias1, bias2);
   char* ws = (char*)workspace;
+  int* flag = (int*)ws;
+  if ((st = numeric_begin(d, flag, cs))) return st;
+  const evo::Shape s = make_shape(d, bias1, bias2, flag);
   float* delta = (float*)(ws + w.delta);
   // fp32 reduction targets: the caller's buffer when it is fp32, else workspace.
   const bool direct = d->dbias_dtype == EVO_F32;
@@ -248,9 +343,6 @@ evo_status evo_attn_bwd(const evo_attn_desc* d, const void* dout, const void* q,
     if (db2) cudaMemsetAsync(db2, 0, n2 * 4, cs);
     if (db1) cudaMemsetAsync(db1, 0, n1 * 4, cs);
   }
-  const bool tc_bwd = path == EVO_PATH_TCGEN05 && evo::tc::bwd_available(d);
-  if (d->dbias2_multicast && !tc_bwd)
-    return fail(EVO_ERR_UNSUPPORTED, "the multicast dBias2 reduction needs the tcgen05 backward (16-bit, D 16/32, L % 8 == 0)");
   if (tc_bwd) {
     // the tcgen05 preamble computes delta itself
     st = evo::tc::bwd(d, s, dout, q, k, v, o, lse, nullptr, dq, dk, dv, db1, db2, ws + w.tc, cs,
@@ -261,15 +353,17 @@ evo_status evo_attn_bwd(const evo_attn_desc* d, const void* dout, const void* q,
       case EVO_BF16: launch_delta<__nv_bfloat16>(s, dout, o, delta, cs); break;
       default: launch_delta<__half>(s, dout, o, delta, cs); break;
     }
+    float* db1p = (float*)(ws + w.db1p);
+    float* db2p = (float*)(ws + w.db2p);
     switch (d->dtype) {
       case EVO_F32:
-        st = simt_bwd_dispatch<float>(s, dout, q, k, v, lse, delta, dq, dk, dv, db1, db2, cs);
+        st = simt_bwd_dispatch<float>(d, s, dout, q, k, v, lse, delta, dq, dk, dv, db1, db2, db1p, db2p, cs);
         break;
       case EVO_BF16:
-        st = simt_bwd_dispatch<__nv_bfloat16>(s, dout, q, k, v, lse, delta, dq, dk, dv, db1, db2, cs);
+        st = simt_bwd_dispatch<__nv_bfloat16>(d, s, dout, q, k, v, lse, delta, dq, dk, dv, db1, db2, db1p, db2p, cs);
         break;
       default:
-        st = simt_bwd_dispatch<__half>(s, dout, q, k, v, lse, delta, dq, dk, dv, db1, db2, cs);
+        st = simt_bwd_dispatch<__half>(d, s, dout, q, k, v, lse, delta, dq, dk, dv, db1, db2, db1p, db2p, cs);
         break;
     }
   }
@@ -283,7 +377,7 @@ evo_status evo_attn_bwd(const evo_attn_desc* d, const void* dout, const void* q,
       if (db1) launch_convert<__half>(db1, dbias1, n1, cs);
     }
   }
-  return check_launch();
+  return numeric_end(d, flag, cs, "dO or the recomputed gradients contain NaN / non-finite values");
 }
 
 }  // extern "C"

@@ -103,10 +103,16 @@ __global__ void __launch_bounds__(Tiles<DP>::kRows) fwd_kernel(Shape s, const T*
   if (!valid) return;
   const float inv = l > 0.f ? 1.f / l : 0.f;
   T* orow = o + row_off(s, b, i, h);
+  bool nan = false;
 #pragma unroll
   for (int d = 0; d < DP; ++d)
-    if (d < s.D) orow[d] = from_f<T>(acc[d] * inv);
-  lse[((size_t)b * s.H + h) * s.L + i] = l > 0.f ? (m + __log2f(l)) * kLn2 : -INFINITY;
+    if (d < s.D) {
+      orow[d] = from_f<T>(acc[d] * inv);
+      nan |= isnan(acc[d]);
+    }
+  const float lv = l > 0.f ? (m + __log2f(l)) * kLn2 : -INFINITY;
+  lse[((size_t)b * s.H + h) * s.L + i] = lv;
+  flag_if(s.flag, nan || !isfinite(lv));
 }
 
 // ------------------------------------------------------- backward: delta
@@ -127,6 +133,7 @@ __global__ void delta_kernel(Shape s, const T* __restrict__ dout, const T* __res
     float acc = 0.f;
     for (int d = 0; d < s.D; ++d) acc = fmaf(to_f(a[d]), to_f(c[d]), acc);
     delta[(b * s.H + h) * s.L + i] = acc;
+    flag_if(s.flag, !isfinite(acc));  // NaN in dO (attention_tiled.cpp:209) or O
   }
 }
 
@@ -135,7 +142,12 @@ template <typename T, int DP>
 __global__ void __launch_bounds__(Tiles<DP>::kRows) dkdv_kernel(
     Shape s, const T* __restrict__ q, const T* __restrict__ k, const T* __restrict__ v,
     const T* __restrict__ dout, const float* __restrict__ lse, const float* __restrict__ delta,
-    T* __restrict__ dk, T* __restrict__ dv, float* __restrict__ dbias1, float* __restrict__ dbias2) {
+    T* __restrict__ dk, T* __restrict__ dv, int b0, float* __restrict__ db1_part, float* __restrict__ db2_part) {
+  // Rows [b0, b0 + gridDim.z) of one outer batch. dBias2 is not added with atomics: every (row, i, j)
+  // term dS is stored once into the row's partial plane db2_part[b - b0][h] (rows of a launch are
+  // never reduced concurrently), and ordered_sum_kernel adds the planes in ascending row order into
+  // the fp32 accumulator — attention_tiled.cpp:246-252, 318-323 with the deterministic (ascending b)
+  // policy. dBias1 partials per head: db1_part[h][b - b0][j], summed over h in order.
   constexpr int kRows = Tiles<DP>::kRows;
   __shared__ float kv[2][kRows][DP + 1];
   __shared__ float qs[kQTile][DP];
@@ -144,7 +156,7 @@ __global__ void __launch_bounds__(Tiles<DP>::kRows) dkdv_kernel(
   const int tid = threadIdx.x;
   const int j = blockIdx.x * kRows + tid;
   const int h = blockIdx.y;
-  const int b = blockIdx.z;
+  const int b = b0 + blockIdx.z;
   const bool valid = j < s.L;
   const int ob = b / s.N;
   for (int x = tid; x < kRows * DP; x += kRows) {
@@ -155,7 +167,7 @@ __global__ void __launch_bounds__(Tiles<DP>::kRows) dkdv_kernel(
   }
   const float b1j = (s.bias1 && valid) ? to_f(static_cast<const T*>(s.bias1)[(size_t)b * s.L + j]) * kLog2e : 0.f;
   const T* b2 = s.bias2 ? static_cast<const T*>(s.bias2) + ((size_t)ob * s.H + h) * s.L * s.L : nullptr;
-  float* db2 = dbias2 ? dbias2 + ((size_t)ob * s.H + h) * s.L * s.L : nullptr;
+  float* db2 = db2_part ? db2_part + ((size_t)blockIdx.z * s.H + h) * s.L * s.L : nullptr;
   float dka[DP], dva[DP];
 #pragma unroll
   for (int d = 0; d < DP; ++d) dka[d] = dva[d] = 0.f;
@@ -196,19 +208,22 @@ __global__ void __launch_bounds__(Tiles<DP>::kRows) dkdv_kernel(
         dka[d] = fmaf(ds, qs[ii][d], dka[d]);
       }
       db1 += ds;
-      if (db2) atomicAdd(db2 + (size_t)i * s.L + j, ds);
+      if (db2) db2[(size_t)i * s.L + j] = ds;
     }
   }
   if (!valid) return;
   T* dkr = dk + row_off(s, b, j, h);
   T* dvr = dv + row_off(s, b, j, h);
+  bool nan = false;
 #pragma unroll
   for (int d = 0; d < DP; ++d)
     if (d < s.D) {
       dkr[d] = from_f<T>(dka[d] * s.scale);
       dvr[d] = from_f<T>(dva[d]);
+      nan |= isnan(dka[d]) || isnan(dva[d]);
     }
-  if (dbias1) atomicAdd(dbias1 + (size_t)b * s.L + j, db1);
+  flag_if(s.flag, nan);
+  if (db1_part) db1_part[((size_t)h * gridDim.z + blockIdx.z) * s.L + j] = db1;
 }
 
 // ------------------------------------------------- backward: dQ (query side)
@@ -216,7 +231,7 @@ template <typename T, int DP>
 __global__ void __launch_bounds__(Tiles<DP>::kRows) dq_kernel(
     Shape s, const T* __restrict__ q, const T* __restrict__ k, const T* __restrict__ v,
     const T* __restrict__ dout, const float* __restrict__ lse, const float* __restrict__ delta,
-    T* __restrict__ dq) {
+    T* __restrict__ dq, int b0) {
   constexpr int kRows = Tiles<DP>::kRows, kKeyTile = Tiles<DP>::kKeyTile;
   __shared__ float ks[kKeyTile][DP];
   __shared__ float vs[kKeyTile][DP];
@@ -225,7 +240,7 @@ __global__ void __launch_bounds__(Tiles<DP>::kRows) dq_kernel(
   const int tid = threadIdx.x;
   const int i = blockIdx.x * kRows + tid;
   const int h = blockIdx.y;
-  const int b = blockIdx.z;
+  const int b = b0 + blockIdx.z;
   const bool valid = i < s.L;
   const int ob = b / s.N;
   for (int x = tid; x < kRows * DP; x += kRows) {
@@ -274,9 +289,14 @@ __global__ void __launch_bounds__(Tiles<DP>::kRows) dq_kernel(
   }
   if (!valid) return;
   T* r = dq + row_off(s, b, i, h);
+  bool nan = false;
 #pragma unroll
   for (int d = 0; d < DP; ++d)
-    if (d < s.D) r[d] = from_f<T>(dqa[d] * s.scale);
+    if (d < s.D) {
+      r[d] = from_f<T>(dqa[d] * s.scale);
+      nan |= isnan(dqa[d]);
+    }
+  flag_if(s.flag, nan);
 }
 
 }  // namespace simt

@@ -103,6 +103,17 @@ struct Params {
   uint32_t aug_c;      // (c_lo << 16) | c_hi: 16-bit split of 1/scale
   unsigned long long* trace;  // bring-up timeline of CTA 0 (null in production)
   int swapped;  // 1: q/k/v/o/dO/dQ/dK/dV are [L, B, H, D] (raw msa_col / tri_end layout)
+  // Row window of this launch: rows n in [n0w, n0w + nw) of every outer batch (items walk the window;
+  // the deterministic mode bounds its partial buffers by launching window after window)
+  int n0w, nw;
+  // Deterministic mode (AccumPolicy::deterministic, attention_tiled.cpp:246-252): dQ partials of each
+  // key tile and the chunked dK/dV partials are TMA-STORED to per-tile / per-chunk slots (window rows
+  // jt*Bw + wrow) and summed in order after the kernel; dBias1 partials go to db1_part; the dBias2
+  // strip flushes of the CTAs sharing a unit are serialised by part through `tickets`.
+  int det;
+  int* tickets;     // [units of the window]: strip flushes done (kSoftWG per part), zeroed by the preamble
+  float* db1_part;  // [H * nIC][Bw][L] when det and dbias1
+  int* flag;        // numeric-check flag (NaN dK / dV) or null
 };
 
 // CTA-0 timeline of steps [kTrFirst, kTrFirst + 64): 8 events x 64 steps (bring-up aid)
@@ -125,18 +136,18 @@ struct Walker {
 __device__ __forceinline__ Walker make_walker(const Params& p) {
   if (p.aligned) {
     const long long unit = blockIdx.x / p.split, part = blockIdx.x % p.split;
-    const long long base = unit * p.N;
-    return Walker{base + p.N * part / p.split, base + p.N * (part + 1) / p.split, p.N};
+    const long long base = unit * p.nw;
+    return Walker{base + p.nw * part / p.split, base + p.nw * (part + 1) / p.split, p.nw};
   }
-  return Walker{p.total * blockIdx.x / gridDim.x, p.total * (blockIdx.x + 1) / gridDim.x, p.N};
+  return Walker{p.total * blockIdx.x / gridDim.x, p.total * (blockIdx.x + 1) / gridDim.x, p.nw};
 }
 struct Unit {
   int ob, h, jt, ic, it0, it1, n0;  // query tiles [it0, it1) of chunk ic
 };
 __device__ __forceinline__ Unit unit_of(long long s0, const Params& p) {
   Unit u;
-  long long x = s0 / p.N;
-  u.n0 = (int)(s0 - x * p.N);
+  long long x = s0 / p.nw;
+  u.n0 = (int)(s0 - x * p.nw);  // window-local row
   u.ic = (int)(x % p.nIC);
   x /= p.nIC;
   u.jt = (int)(x % p.nKT);
@@ -152,6 +163,21 @@ __device__ __forceinline__ uint4 lds128(uint32_t a) {
   uint4 v;
   asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(a));
   return v;
+}
+__device__ __forceinline__ int ld_acquire(const int* p) {
+  int v;
+  asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+// Index of this CTA among the CTAs whose item ranges intersect `unit` (0 = the first): the flush
+// order of the deterministic dBias2 reduction.
+__device__ __forceinline__ int unit_part(const Params& p, long long unit) {
+  if (p.aligned) return (int)(blockIdx.x % p.split);
+  const long long first = unit * p.nw;  // first item of the unit; CTA c covers [total*c/G, total*(c+1)/G)
+  long long c = first * gridDim.x / p.total;
+  while (c > 0 && p.total * c / gridDim.x > first) --c;
+  while (p.total * (c + 1) / gridDim.x <= first) ++c;
+  return (int)(blockIdx.x - c);
 }
 __device__ __forceinline__ void sts128(uint32_t a, uint4 v) {
   asm volatile("st.shared.v4.u32 [%0], {%1,%2,%3,%4};" ::"r"(a), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w) : "memory");
@@ -302,7 +328,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         int n = u.n0;
         for (int a = 0; a < cnt; ++a, ++n) {
-          const int b = u.ob * p.N + n;
+          const int b = u.ob * p.N + p.n0w + n;
           // K, V (and the bias1 chunk) of this row's key tile
           ptx::mbar_wait(&k_empty[ks], kph ^ 1);
           const int nk = min(kBN, p.L - u.jt * kBN);  // keys of this tile (multiple of 8)
@@ -589,6 +615,13 @@ __global__ void __launch_bounds__(kThreads, 1)
         ptx::mbar_wait(strip_full, uph);
         uph ^= 1;
         ptx::tc_fence_after();
+        const long long unit = s0 / p.nw;
+        if (p.det) {  // the unit's CTAs flush in part order: wait for the lower parts' warpgroups
+          const int part = unit_part(p, unit);
+          if (tid_wg == 0)
+            while (ld_acquire(p.tickets + unit) < part * kSoftWG) __nanosleep(64);
+          ptx::named_bar_sync(1 + wg, 128);
+        }
         const int j0 = u.jt * kBN + (int)col;
         for (int it = (CH ? u.it0 : 0); it < (CH ? u.it1 : p.nQT); ++it) {
           const int i = it * kBM + r;
@@ -609,6 +642,11 @@ __global__ void __launch_bounds__(kThreads, 1)
               }
           }
         }
+      }
+      if (p.dbias2 && p.det) {  // this warpgroup's adds are performed before the next part may start
+        __threadfence();
+        ptx::named_bar_sync(1 + wg, 128);
+        if (tid_wg == 0) atomicAdd(p.tickets + s0 / p.nw, 1);
       }
       if (p.dbias2) ptx::tc_fence_before();  // strip reads ordered before the next P/dS arrival (its MMAs overwrite)
       if (p.dbias2 && p.dbias2_mc) __threadfence_system();  // remote adds ordered before the ranks' barrier
@@ -631,7 +669,9 @@ __global__ void __launch_bounds__(kThreads, 1)
       const Unit u = unit_of(s0, p);
       int n = u.n0;
       for (int a = 0; a < cnt; ++a, ++n) {
-        const int b = u.ob * p.N + n;
+        const int b = u.ob * p.N + p.n0w + n;
+        const int wrow = u.ob * p.nw + n;  // row of the window (deterministic partial slots)
+        const int Bw = p.Bo * p.nw;
         for (int it = (CH ? u.it0 : 0); it < (CH ? u.it1 : p.nQT); ++it) {
           // ---- dQ partial: TMEM -> staging (fp32, swizzled rows) -> TMA reduce-add into dQacc
           ptx::mbar_wait(dq_full, step & 1);
@@ -658,7 +698,8 @@ __global__ void __launch_bounds__(kThreads, 1)
           ptx::fence_proxy_async_smem();
           ptx::named_bar_sync(kEpiBar, 128);
           if (tid_e == 0) {
-            ptx::tma_reduce_add_4d(&tmdQ, stg, 0, u.h, it * kBM, b);
+            if (p.det) ptx::tma_store_4d(&tmdQ, stg, 0, u.h, it * kBM, u.jt * Bw + wrow);  // key tile jt's slot
+            else ptx::tma_reduce_add_4d(&tmdQ, stg, 0, u.h, it * kBM, b);
             ptx::bulk_commit();
             trace(p, kTbDqOut, step);
           }
@@ -677,7 +718,10 @@ __global__ void __launch_bounds__(kThreads, 1)
         ptx::mbar_arrive(kv_free);
         if (p.dbias1 && lane < 16) {  // lanes 0-15 of quadrant q4 hold keys q4*16 + lane (M=64 layout)
           const int jj = u.jt * kBN + q4 * 16 + lane;
-          if (jj < p.L) atomicAdd(p.dbias1 + (size_t)b * p.L + jj, __uint_as_float(b1v[0]));
+          if (jj < p.L) {
+            if (p.det) p.db1_part[(((size_t)u.h * p.nIC + u.ic) * Bw + wrow) * p.L + jj] = __uint_as_float(b1v[0]);
+            else atomicAdd(p.dbias1 + (size_t)b * p.L + jj, __uint_as_float(b1v[0]));
+          }
         }
         ++rows;
         const int krow = q4 * 16 + (lane & 15);
@@ -699,8 +743,13 @@ __global__ void __launch_bounds__(kThreads, 1)
           ptx::fence_proxy_async_smem();
           ptx::named_bar_sync(kEpiBar, 128);
           if (tid_e == 0) {
-            ptx::tma_reduce_add_4d(&tmdK, stg, 0, u.h, u.jt * kBN, b);
-            ptx::tma_reduce_add_4d(&tmdV, stg + 64 * D, 0, u.h, u.jt * kBN, b);
+            if (p.det) {  // chunk ic's slot
+              ptx::tma_store_4d(&tmdK, stg, 0, u.h, u.jt * kBN, u.ic * Bw + wrow);
+              ptx::tma_store_4d(&tmdV, stg + 64 * D, 0, u.h, u.jt * kBN, u.ic * Bw + wrow);
+            } else {
+              ptx::tma_reduce_add_4d(&tmdK, stg, 0, u.h, u.jt * kBN, b);
+              ptx::tma_reduce_add_4d(&tmdV, stg + 64 * D, 0, u.h, u.jt * kBN, b);
+            }
             ptx::bulk_commit();
             ptx::bulk_wait_read<0>();  // the buffer is the next dQ step's
           }
@@ -708,6 +757,12 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         const int j = u.jt * kBN + krow;
         if (j < p.L) {
+          if (p.flag) {
+            bool nan = false;
+#pragma unroll
+            for (int d = 0; d < D; ++d) nan |= isnan(__uint_as_float(v[d]));
+            flag_if(p.flag, nan);
+          }
           const float sc = isk ? p.scale : 1.f;
           uint32_t ow[D / 2];
 #pragma unroll
@@ -738,7 +793,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 template <int D, typename T, bool SW>
 __global__ void prep_kernel(const T* __restrict__ dout, const T* __restrict__ o, const float* __restrict__ lse,
                             float* __restrict__ lse2, float* __restrict__ delta_p, int B, int L, int H, int Lp,
-                            float4* __restrict__ zero, long long nzero4) {
+                            float4* __restrict__ zero, long long nzero4, int* __restrict__ flag) {
   constexpr bool swapped = SW;
   ptx::pdl_launch_dependents();
   for (long long x = blockIdx.x * (long long)blockDim.x + threadIdx.x; x < nzero4; x += (long long)gridDim.x * blockDim.x)
@@ -768,6 +823,7 @@ __global__ void prep_kernel(const T* __restrict__ dout, const T* __restrict__ o,
       for (int e = 0; e < 8; ++e) acc = fmaf(to_f(ue[e]), to_f(we[e]), acc);
     }
     delta_p[orow] = acc;
+    flag_if(flag, !isfinite(acc));  // NaN in dO (attention_tiled.cpp:209) or O
     lse2[orow] = lse[((size_t)b * H + h) * L + i] * kLog2e;
   }
 }
@@ -801,7 +857,7 @@ __device__ __forceinline__ size_t out_off(size_t x, int B, int L, int HD, int sw
 // acc is canonical [B, L, H, D]; swapped writes the [L, B, H, D] layout (8-element groups stay in one row)
 template <typename T, bool SW>
 __global__ void dq_convert_kernel(const float* __restrict__ acc, T* __restrict__ dq, size_t n, float scale,
-                                  int B, int L, int HD) {
+                                  int B, int L, int HD, int* __restrict__ flag) {
   constexpr int swapped = SW;
   ptx::pdl_wait();  // programmatic dependent of the main kernel
   ptx::pdl_launch_dependents();
@@ -813,12 +869,59 @@ __global__ void dq_convert_kernel(const float* __restrict__ acc, T* __restrict__
   }
   for (size_t x = (blockIdx.x * (size_t)blockDim.x + threadIdx.x) * 8; x < n; x += (size_t)gridDim.x * blockDim.x * 8) {
     const float4 a = __ldcs((const float4*)(acc + x)), c = __ldcs((const float4*)(acc + x + 4));
+    if (flag)
+      flag_if(flag, isnan(a.x) || isnan(a.y) || isnan(a.z) || isnan(a.w) || isnan(c.x) || isnan(c.y) || isnan(c.z) ||
+                        isnan(c.w));
     uint4 w;
     w.x = F16 ? ptx::pack_f16(a.x * scale, a.y * scale) : ptx::pack_bf16(a.x * scale, a.y * scale);
     w.y = F16 ? ptx::pack_f16(a.z * scale, a.w * scale) : ptx::pack_bf16(a.z * scale, a.w * scale);
     w.z = F16 ? ptx::pack_f16(c.x * scale, c.y * scale) : ptx::pack_bf16(c.x * scale, c.y * scale);
     w.w = F16 ? ptx::pack_f16(c.z * scale, c.w * scale) : ptx::pack_bf16(c.z * scale, c.w * scale);
     *(uint4*)(dq + out_off(x, B, L, HD, swapped)) = w;
+  }
+}
+
+// Deterministic mode: out = scale * (part[0] + part[1] + ... + part[np-1]) for the rows of one window,
+// the partial slots (key tiles for dQ, query chunks for dK / dV) added in ascending order — the
+// fixed-order reduction that makes two runs bit-identical. Element x of the window: window row
+// wrow = ob * nw + r is canonical row b = ob * N + n0w + r; 8 elements per thread (HD % 8 == 0).
+template <typename T, bool SW>
+__global__ void det_convert_kernel(const float* __restrict__ part, int np, size_t pstride, T* __restrict__ out,
+                                   size_t n, float scale, int B, int L, int HD, int N, int n0w, int nw,
+                                   int* __restrict__ flag) {
+  ptx::pdl_wait();  // programmatic dependent of the main kernel
+  ptx::pdl_launch_dependents();
+  constexpr bool F16 = std::is_same<T, __half>::value;
+  const size_t rowlen = (size_t)L * HD;
+  for (size_t x = (blockIdx.x * (size_t)blockDim.x + threadIdx.x) * 8; x < n; x += (size_t)gridDim.x * blockDim.x * 8) {
+    float a[8];
+    {
+      const float4 u = *(const float4*)(part + x), w = *(const float4*)(part + x + 4);
+      a[0] = u.x; a[1] = u.y; a[2] = u.z; a[3] = u.w; a[4] = w.x; a[5] = w.y; a[6] = w.z; a[7] = w.w;
+    }
+    for (int k = 1; k < np; ++k) {
+      const float4 u = *(const float4*)(part + (size_t)k * pstride + x), w = *(const float4*)(part + (size_t)k * pstride + x + 4);
+      a[0] += u.x; a[1] += u.y; a[2] += u.z; a[3] += u.w; a[4] += w.x; a[5] += w.y; a[6] += w.z; a[7] += w.w;
+    }
+    bool nan = false;
+    uint32_t wv[4];
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      nan |= isnan(a[2 * e]) || isnan(a[2 * e + 1]);
+      wv[e] = F16 ? ptx::pack_f16(a[2 * e] * scale, a[2 * e + 1] * scale)
+                  : ptx::pack_bf16(a[2 * e] * scale, a[2 * e + 1] * scale);
+    }
+    flag_if(flag, nan);
+    const size_t wrow = x / rowlen, rem = x - wrow * rowlen;
+    const size_t ob = wrow / nw, b = ob * N + n0w + (wrow - ob * nw);
+    const size_t i = rem / HD, e = rem - i * HD;
+    const size_t off = SW ? (i * B + b) * HD + e : (b * L + i) * HD + e;
+    if (((uintptr_t)(out + off) & 15) == 0) {
+      *(uint4*)(out + off) = make_uint4(wv[0], wv[1], wv[2], wv[3]);
+    } else {
+      const uint16_t* hv = (const uint16_t*)wv;
+      for (int q = 0; q < 8; ++q) ((uint16_t*)out)[off + q] = hv[q];
+    }
   }
 }
 

@@ -64,6 +64,8 @@ struct FwdParams {
   int b1_tma;        // bias1 rows fetched by TMA bulk copy (L % 8 == 0)
   int aug;           // bias1 / key mask enter S as one extra K=16 MMA step (bias1 present or L % 64 != 0)
   uint32_t aug_c;    // (c_lo << 16) | c_hi: 16-bit two-term split of 1/scale
+  int b1_rows;       // bias1 rows staged in shared memory per Q slot (b1_tma and the budget allows)
+  int* flag;         // numeric-check flag (non-finite LSE / NaN O) or null
   const void* bias1;  // [B, L] or null
   const void* bias2;  // [Bo, H, L, L] (read directly in kBiasGlobal mode)
   void* o;           // [B, L, H, D]
@@ -157,8 +159,8 @@ __global__ void __launch_bounds__(FwdCfg<D>::kThreads, 1)
   uint8_t* sBias = sV + C::kStages * C::kTileKV;            // [nbias_slots] x 16 KB
   uint8_t* sAaug = sBias + (size_t)p.nbias_slots * C::kBiasTile;  // 128 x 16: (c_hi, c_lo, 0..), SW32
   uint8_t* sBaug = sAaug + kAugA;                            // [stages] 64 x 16: (bias1, bias1, 0..), SW32
-  uint16_t* sB1raw = (uint16_t*)(sBaug + C::kStages * kAugB);  // [NWG][2][LP] bias1 rows (raw)
-  uint64_t* bars = (uint64_t*)(sB1raw + NWG * 2 * LP);
+  uint16_t* sB1raw = (uint16_t*)(sBaug + C::kStages * kAugB);  // [NWG][2][LP] bias1 rows (raw), when b1_rows
+  uint64_t* bars = (uint64_t*)(sB1raw + (p.b1_rows ? NWG * 2 * LP : 0));
   uint64_t* q_full = bars;                       // [NWG][2] Q (+ bias1 row) landed
   uint64_t* q_empty = q_full + 2 * NWG;          // [NWG][2] last S of the row done
   uint64_t* s_full = q_empty + 2 * NWG;          // [NWG][2]
@@ -228,7 +230,7 @@ __global__ void __launch_bounds__(FwdCfg<D>::kThreads, 1)
       for (int w = 0; w < NWG; ++w) qc[w] = tk[w] = 0;
       int bslot = 0; uint32_t bph = 0;
       const uint32_t b1_bytes = (uint32_t)p.L * 2;
-      const bool b1t = p.bias1 && p.b1_tma;
+      const bool b1t = p.bias1 && p.b1_rows;
       for (long long s0 = W.t0; s0 < W.t1; s0 = W.seg_end(s0)) {
         const long long s1 = W.seg_end(s0);
         const SegInfo si = seg_info(s0, p);
@@ -379,7 +381,7 @@ __global__ void __launch_bounds__(FwdCfg<D>::kThreads, 1)
                 if (key >= p.L) {
                   v0 = F16 ? 0xFC00u : 0xFF80u;
                 } else if (p.bias1) {
-                  v0 = p.b1_tma ? (uint32_t)sB1raw[(w * 2 + qs) * LP + key]
+                  v0 = p.b1_rows ? (uint32_t)sB1raw[(w * 2 + qs) * LP + key]
                                 : (uint32_t)((const uint16_t*)p.bias1)[(size_t)b * p.L + key];
                   const bool fin = F16 ? (v0 & 0x7C00u) != 0x7C00u : (v0 & 0x7F80u) != 0x7F80u;
                   v1 = fin ? v0 : 0u;
@@ -594,7 +596,14 @@ __global__ void __launch_bounds__(FwdCfg<D>::kThreads, 1)
                                  ((p.swapped ? (size_t)i * p.B + b : (size_t)b * p.L + i) * p.H + si.h) * D);
 #pragma unroll
           for (int v = 0; v < D / 8; ++v) dst[v] = make_uint4(ow[4 * v], ow[4 * v + 1], ow[4 * v + 2], ow[4 * v + 3]);
-          p.lse[((size_t)b * p.H + si.h) * p.L + i] = l_run > 0.f ? (m_run + __log2f(l_run)) * kLn2 : -INFINITY;
+          const float lv = l_run > 0.f ? (m_run + __log2f(l_run)) * kLn2 : -INFINITY;
+          p.lse[((size_t)b * p.H + si.h) * p.L + i] = lv;
+          if (p.flag) {  // NumericError: a NaN input or no finite logit in the row
+            bool nan = !isfinite(lv);
+#pragma unroll
+            for (int d = 0; d < D; ++d) nan |= isnan(__uint_as_float(ov[d]));
+            flag_if(p.flag, nan);
+          }
         }
       }
       if (resident) {

@@ -3,7 +3,9 @@
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
+#include <cmath>
 #include <cstdio>
+#include <cstring>
 #include <cstdlib>
 #include <mutex>
 
@@ -84,14 +86,14 @@ bool map_bias(CUtensorMap* m, const void* base, const Shape& s, int Bo, CUtensor
 }
 
 template <int D>
-size_t fwd_smem_bytes(int nbias_slots, int nKT) {
+size_t fwd_smem_bytes(int nbias_slots, int nKT, bool b1_rows) {
   using C = FwdCfg<D>;
   const size_t LP = (size_t)nKT * kBN;
   size_t b = 1024;  // alignment slack
   b += (size_t)C::NWG * 2 * C::kTileQ + 2 * (size_t)C::kStages * C::kTileKV;
   b += (size_t)nbias_slots * C::kBiasTile;
   b += (size_t)kAugA + (size_t)C::kStages * kAugB;  // bias1 augmentation tiles
-  b += (size_t)C::NWG * 2 * LP * 2;                 // bias1 rows (raw), double buffered per WG
+  if (b1_rows) b += (size_t)C::NWG * 2 * LP * 2;  // bias1 rows (raw), double buffered per WG
   b += (size_t)(11 * C::NWG + 4 * C::kStages + 2 * nbias_slots) * 8 + 16;
   return b;
 }
@@ -142,12 +144,16 @@ evo_status launch_fwd(const evo_attn_desc* d, const Shape& s, const void* q, con
   p.b1_tma = (s.L % 8 == 0) ? 1 : 0;
   p.aug = (s.bias1 != nullptr || s.L % kBN != 0) ? 1 : 0;
   p.aug_c = aug_split(1.0 / (double)s.scale, F16);
+  p.flag = s.flag;
+  // bias1 rows staged per Q slot when they are bulk-copyable and fit; otherwise the UMMA warp reads
+  // them from global (long L)
+  p.b1_rows = (s.bias1 && p.b1_tma && fwd_smem_bytes<D>(3, p.nKT, true) <= kMaxSmem) ? 1 : 0;
   if (s.bias2) {
     if (s.L % 8 != 0) {
       p.bias_mode = kBiasGlobal;
     } else {
       if (!map_bias(&tb, s.bias2, s, p.Bo, dt, err)) return EVO_ERR_CUDA;
-      if (fwd_smem_bytes<D>(p.nKT, p.nKT) <= kMaxSmem) {
+      if (fwd_smem_bytes<D>(p.nKT, p.nKT, p.b1_rows) <= kMaxSmem) {
         p.bias_mode = kBiasResident;
         p.nbias_slots = p.nKT;
       } else {
@@ -156,7 +162,7 @@ evo_status launch_fwd(const evo_attn_desc* d, const Shape& s, const void* q, con
       }
     }
   }
-  const size_t smem = fwd_smem_bytes<D>(p.nbias_slots, p.nKT);
+  const size_t smem = fwd_smem_bytes<D>(p.nbias_slots, p.nKT, p.b1_rows);
   if (smem > kMaxSmem) {
     *err = "forward shared-memory budget exceeded (L too large)";
     return EVO_ERR_UNSUPPORTED;
@@ -185,11 +191,9 @@ evo_status launch_fwd(const evo_attn_desc* d, const Shape& s, const void* q, con
 }
 
 // ---------------------------------------------------------------------------------- backward
-struct BwdScratch {
-  size_t dq, dk, dv, lse2, delta, total;  // dk/dv: fp32 accumulators, only when L spans several query chunks
-};
 constexpr int kBwdChunk = 3;  // query tiles per backward unit: its dBias2 strip (3 x 64 TMEM columns) fits
 int bwd_nqt(const evo_attn_desc* d) { return (int)((d->L + bk::kBM - 1) / bk::kBM); }
+int bwd_nkt(const evo_attn_desc* d) { return (int)((d->L + bk::kBN - 1) / bk::kBN); }
 // dBias1 needs 16 TMEM columns: its chunks hold 2 query tiles (strip 128 columns) instead of 3
 // without a pair bias there is no dBias2 strip in TMEM and no bias strip in shared memory: the whole
 // query axis is one chunk at any L (MSA column attention: bias-free plus mask, L = N_seq)
@@ -201,20 +205,70 @@ int bwd_nic(const evo_attn_desc* d, bool db1 = false) {
   return (bwd_nqt(d) + c - 1) / c;
 }
 size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
+
+// Scratch of the tcgen05 backward.
+//  default:       fp32 accumulators dQ (and dK, dV when the query axis is chunked) [B, L, H, D]
+//                 (zeroed by the preamble, TMA reduce-add targets), padded lse*log2e and delta.
+//  deterministic: per-slot partials of one row window — dQ [nKT][Bw, L, H, D], chunked dK / dV
+//                 [nIC][Bw, L, H, D], dBias1 [H * nIC][Bw][L] — plus the dBias2 flush tickets of
+//                 every window; windows of nw rows per outer batch keep the partials under kDetCap.
+constexpr size_t kDetCap = (size_t)2 << 30;
+struct BwdScratch {
+  size_t dq, dk, dv, lse2, delta, db1p, tickets, total;
+  int nw, nwin;  // deterministic row window (rows per outer batch), number of windows
+};
 BwdScratch bwd_scratch_layout(const evo_attn_desc* d) {
   BwdScratch w{};
   const size_t B = (size_t)d->Bo * d->N;
-  const size_t Lp = (size_t)((d->L + bk::kBM - 1) / bk::kBM) * bk::kBM;
-  const size_t acc = align256(B * d->L * d->H * d->D * 4);
+  const size_t Lp = (size_t)bwd_nqt(d) * bk::kBM;
+  const size_t row = (size_t)d->L * d->H * d->D * 4;  // one row's fp32 [L, H, D]
+  const bool db1 = d->has_bias1 && d->need_dbias1;
+  const int nic = bwd_nic(d, db1), nkt = bwd_nkt(d);
+  const bool chunked = nic > 1;
+  w.nw = (int)d->N;
+  w.nwin = 1;
+  size_t dq_bytes, kv_bytes, db1p = 0, tickets = 0;
+  if (d->deterministic) {
+    const size_t per = row * ((size_t)nkt + (chunked ? 2 * (size_t)nic : 0)) + (db1 ? (size_t)d->H * nic * d->L * 4 : 0);
+    w.nw = (int)std::max<int64_t>(1, std::min<int64_t>(d->N, (int64_t)(kDetCap / (per * d->Bo))));
+    if (const char* e = getenv("EVO_DET_WINDOW_ROWS"))  // test hook: force smaller row windows
+      if (atoi(e) > 0) w.nw = std::min(w.nw, atoi(e));
+    w.nwin = (int)((d->N + w.nw - 1) / w.nw);
+    const size_t Bw = (size_t)d->Bo * w.nw;
+    dq_bytes = align256((size_t)nkt * Bw * row);
+    kv_bytes = chunked ? align256((size_t)nic * Bw * row) : 0;
+    db1p = db1 ? align256((size_t)d->H * nic * Bw * d->L * 4) : 0;
+    tickets = align256((size_t)w.nwin * d->Bo * d->H * nkt * nic * 4);
+  } else {
+    dq_bytes = align256(B * row);
+    kv_bytes = chunked ? dq_bytes : 0;  // dK/dV accumulators when the query axis is chunked
+  }
   w.dq = 0;
-  w.dk = acc;
-  // dK/dV accumulators when the query axis is chunked (a dBias1 request chunks by 2 tiles)
-  const bool may_chunk = bwd_nic(d, d->has_bias1 && d->need_dbias1) > 1;
-  w.dv = w.dk + (may_chunk ? acc : 0);
-  w.lse2 = w.dv + (may_chunk ? acc : 0);
+  w.dk = dq_bytes;
+  w.dv = w.dk + kv_bytes;
+  w.lse2 = w.dv + kv_bytes;
   w.delta = w.lse2 + align256(B * d->H * Lp * 4);
-  w.total = w.delta + align256(B * d->H * Lp * 4);
+  w.db1p = w.delta + align256(B * d->H * Lp * 4);
+  w.tickets = w.db1p + db1p;
+  w.total = w.tickets + tickets;
   return w;
+}
+
+// fp32 [rows, L, H, D] (canonical) as a 4-D map (D, H, L, rows), box (D, 1, box_rows, 1), row-size swizzle
+bool map_f32_rows(CUtensorMap* m, void* base, const Shape& s, long long rows, int box_rows, std::string* err) {
+  cuuint64_t dims[4] = {(cuuint64_t)s.D, (cuuint64_t)s.H, (cuuint64_t)s.L, (cuuint64_t)rows};
+  const cuuint64_t hd = (cuuint64_t)s.H * s.D * 4;
+  cuuint64_t strides[3] = {(cuuint64_t)s.D * 4, hd, hd * (cuuint64_t)s.L};
+  cuuint32_t box[4] = {(cuuint32_t)s.D, 1, (cuuint32_t)box_rows, 1};
+  cuuint32_t es[4] = {1, 1, 1, 1};
+  CUresult r = encode_fn()(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, base, dims, strides, box, es,
+                           CU_TENSOR_MAP_INTERLEAVE_NONE, swz(s.D * 4), CU_TENSOR_MAP_L2_PROMOTION_NONE,
+                           CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) {
+    *err = "cuTensorMapEncodeTiled (fp32 partials) failed: " + std::to_string((int)r);
+    return false;
+  }
+  return true;
 }
 
 template <int D, bool CH>
@@ -236,6 +290,7 @@ evo_status launch_bwd(const evo_attn_desc* d, const Shape& s, const void* dout, 
                       std::string* err) {
   const CUtensorMapDataType dt = F16 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT16 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16;
   const BwdScratch w = bwd_scratch_layout(d);
+  const bool det = d->deterministic != 0;
   char* ws = (char*)scratch;
   float* dqacc = (float*)(ws + w.dq);
   float* lse2 = (float*)(ws + w.lse2);
@@ -246,27 +301,30 @@ evo_status launch_bwd(const evo_attn_desc* d, const Shape& s, const void* dout, 
   const bool dkv_reduce = bwd_nic(d, want_db1) > 1;
   float* dkacc = (float*)(ws + w.dk);
   float* dvacc = (float*)(ws + w.dv);
+  const int nkt = bwd_nkt(d), nic = bwd_nic(d, want_db1);
+  const long long Bw = (long long)d->Bo * w.nw;  // rows of a (full) deterministic window
   if (dkv_reduce) {
-    if (!map_bl_hd(&tdk, dkacc, s, bk::kBN, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, err, true) ||
-        !map_bl_hd(&tdv, dvacc, s, bk::kBN, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, err, true))
-      return EVO_ERR_CUDA;
+    const bool ok = det ? map_f32_rows(&tdk, dkacc, s, nic * Bw, bk::kBN, err) && map_f32_rows(&tdv, dvacc, s, nic * Bw, bk::kBN, err)
+                        : map_bl_hd(&tdk, dkacc, s, bk::kBN, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, err, true) &&
+                              map_bl_hd(&tdv, dvacc, s, bk::kBN, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, err, true);
+    if (!ok) return EVO_ERR_CUDA;
   } else {
     tdk = tdv = tb;
   }
   if (!map_bl_hd(&tq, q, s, bk::kBM, dt, 2, err) || !map_bl_hd(&tk, k, s, bk::kBN, dt, 2, err) ||
       !map_bl_hd(&tv, v, s, bk::kBN, dt, 2, err) || !map_bl_hd(&tdo, dout, s, bk::kBM, dt, 2, err) ||
-      !map_bl_hd(&tdq, dqacc, s, bk::kBM, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, err, true))
+      !(det ? map_f32_rows(&tdq, dqacc, s, nkt * Bw, bk::kBM, err)
+            : map_bl_hd(&tdq, dqacc, s, bk::kBM, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, err, true)))
     return EVO_ERR_CUDA;
   if (s.bias2 && !map_bias(&tb, s.bias2, s, (int)d->Bo, dt, err)) return EVO_ERR_CUDA;
   bk::Params p{};
   p.B = s.B; p.N = s.N; p.L = s.L; p.H = s.H; p.Bo = (int)d->Bo;
   p.swapped = s.swapped;
   p.nQT = (s.L + bk::kBM - 1) / bk::kBM;
-  p.nKT = (s.L + bk::kBN - 1) / bk::kBN;
+  p.nKT = nkt;
   p.nQC = bwd_chunk(d, want_db1);
-  p.nIC = bwd_nic(d, want_db1);
+  p.nIC = nic;
   p.dbias1 = dbias1;
-  p.total = (long long)p.Bo * p.H * p.nKT * p.nIC * p.N;
   p.dkv_reduce = dkv_reduce ? 1 : 0;
   p.scale = s.scale;
   p.scale_log2 = s.scale_log2;
@@ -282,6 +340,9 @@ evo_status launch_bwd(const evo_attn_desc* d, const Shape& s, const void* dout, 
   }
   p.has_bias2 = s.bias2 != nullptr;
   p.trace = g_trace_bwd;
+  p.det = det ? 1 : 0;
+  p.db1_part = (float*)(ws + w.db1p);
+  p.flag = s.flag;
   // bias1 (and the key mask past L) enter S through one extra K=16 MMA step: A_aug rows hold a
   // 16-bit two-term split of 1/scale, B_aug rows the bias1 value of each key.
   p.aug = (s.bias1 != nullptr || s.L % bk::kBN != 0) ? 1 : 0;
@@ -294,9 +355,11 @@ evo_status launch_bwd(const evo_attn_desc* d, const Shape& s, const void* dout, 
   }
   const int Lp = p.nQT * bk::kBM;
   const long long prow = (long long)s.B * s.H;
-  // the preamble also zeroes the dQ (and dK, dV when chunked) fp32 accumulators: [0, w.lse2)
-  float4* zero4 = (float4*)dqacc;
-  const long long nzero4 = (long long)((dkv_reduce ? w.lse2 : w.dk) / 16);  // only the accumulators this call uses
+  // the preamble also zeroes the fp32 accumulators this call reduces into ([0, w.lse2): dQ, and dK / dV
+  // when chunked) — or, deterministic, only the dBias2 flush tickets (partials are stored, not added)
+  float4* zero4 = det ? (float4*)(ws + w.tickets) : (float4*)dqacc;
+  const long long nzero4 = det ? (long long)((w.total - w.tickets) / 16)
+                               : (long long)((dkv_reduce ? w.lse2 : w.dk) / 16);
   using T = typename std::conditional<F16, __half, __nv_bfloat16>::type;
   if (delta) {  // delta supplied by the caller: only pad
     bk::pad_rows_kernel<<<(unsigned)std::min<long long>((prow * Lp + 255) / 256, 148 * 16), 256, 0, st>>>(
@@ -304,56 +367,78 @@ evo_status launch_bwd(const evo_attn_desc* d, const Shape& s, const void* dout, 
   } else {
     auto prep = s.swapped ? bk::prep_kernel<D, T, true> : bk::prep_kernel<D, T, false>;
     prep<<<(unsigned)std::min<long long>((prow * Lp + 255) / 256, 148 * 32), 256, 0, st>>>(
-        (const T*)dout, (const T*)o, lse, lse2, delta_p, s.B, s.L, s.H, Lp, zero4, nzero4);
+        (const T*)dout, (const T*)o, lse, lse2, delta_p, s.B, s.L, s.H, Lp, zero4, nzero4, s.flag);
   }
   ++*launches;
   auto kern = s.swapped ? (dkv_reduce ? bk::bwd_kernel<D, F16, true, true> : bk::bwd_kernel<D, F16, false, true>)
                         : (dkv_reduce ? bk::bwd_kernel<D, F16, true, false> : bk::bwd_kernel<D, F16, false, false>);
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   const int G = sm_count();
-  const long long units = (long long)p.Bo * p.H * p.nKT * p.nIC;
-  long long grid = std::min<long long>(p.total, G);
-  p.aligned = 0;
-  p.split = 1;
-  if (units <= G) {
-    p.split = (int)std::min<long long>(G / units, p.N);
-    p.aligned = 1;
-    grid = units * p.split;
-  }
-  {  // programmatic dependent launch: the prologue overlaps the preamble's tail (pdl_wait inside)
-    cudaLaunchConfig_t cfg = {};
+  auto pdl_launch = [&](auto fn, dim3 grid, dim3 block, size_t shm, auto... args) {
+    cudaLaunchConfig_t cfg = {};  // programmatic dependent launch: the prologue overlaps the predecessor's tail
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     attr[0].val.programmaticStreamSerializationAllowed = 1;
-    cfg.gridDim = dim3((unsigned)grid);
-    cfg.blockDim = dim3(bk::kThreads);
-    cfg.dynamicSmemBytes = smem;
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = shm;
     cfg.stream = st;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    cudaLaunchKernelEx(&cfg, kern, tq, tk, tv, tdo, tb, tdq, tdk, tdv, p);
-  }
-  ++*launches;
-  const size_t n = (size_t)s.B * s.L * s.H * D;
-  const unsigned cg = (unsigned)std::min<size_t>((n / 8 + 255) / 256, 148 * 16);
-  auto convert = [&](const float* acc, void* out, float scale) {  // programmatic dependents of the main kernel
-    cudaLaunchConfig_t cfg = {};
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    attr[0].val.programmaticStreamSerializationAllowed = 1;
-    cfg.gridDim = dim3(cg);
-    cfg.blockDim = dim3(256);
-    cfg.stream = st;
-    cfg.attrs = attr;
-    cfg.numAttrs = 1;
-    cudaLaunchKernelEx(&cfg, s.swapped ? bk::dq_convert_kernel<T, true> : bk::dq_convert_kernel<T, false>, acc,
-                       (T*)out, n, scale, s.B, s.L, s.H * D);
+    cudaLaunchKernelEx(&cfg, fn, args...);
     ++*launches;
   };
-  convert(dqacc, dq, s.scale);
-  if (dkv_reduce) {  // dK = scale * dK_acc, dV = dV_acc
-    convert(dkacc, dk, s.scale);
-    convert(dvacc, dv, 1.f);
+  const long long units = (long long)p.Bo * p.H * p.nKT * p.nIC;
+  const int HD = s.H * D;
+  for (int win = 0; win < w.nwin; ++win) {
+    p.n0w = win * w.nw;
+    p.nw = std::min<int>(w.nw, s.N - p.n0w);
+    p.total = units * p.nw;
+    p.tickets = det ? (int*)(ws + w.tickets) + (size_t)win * units : nullptr;
+    long long grid = std::min<long long>(p.total, G);
+    p.aligned = 0;
+    p.split = 1;
+    if (units <= G) {
+      p.split = (int)std::min<long long>(G / units, p.nw);
+      p.aligned = 1;
+      grid = units * p.split;
+    }
+    pdl_launch(kern, dim3((unsigned)grid), dim3(bk::kThreads), smem, tq, tk, tv, tdo, tb, tdq, tdk, tdv, p);
+    if (det) {
+      // ordered sums of this window's partial slots (dQ over key tiles; dK / dV over query chunks)
+      const size_t n = (size_t)p.Bo * p.nw * s.L * HD, pstride = n;
+      const unsigned cg = (unsigned)std::min<size_t>((n / 8 + 255) / 256, 148 * 16);
+      auto conv = [&](const float* part, int np, void* out, float scale) {
+        pdl_launch(s.swapped ? bk::det_convert_kernel<T, true> : bk::det_convert_kernel<T, false>, dim3(cg), dim3(256),
+                   0, part, np, pstride, (T*)out, n, scale, s.B, s.L, HD, s.N, p.n0w, p.nw, s.flag);
+      };
+      conv(dqacc, nkt, dq, s.scale);
+      if (dkv_reduce) {
+        conv(dkacc, nic, dk, s.scale);
+        conv(dvacc, nic, dv, 1.f);
+      }
+      if (dbias1) {  // dBias1 partials of (head, chunk) slots in order, per outer batch of the window
+        const size_t nl = (size_t)p.nw * s.L;
+        for (int ob = 0; ob < p.Bo; ++ob) {
+          ordered_sum_kernel<float><<<(unsigned)std::min<size_t>((nl + 255) / 256, 148 * 4), 256, 0, st>>>(
+              p.db1_part + (size_t)ob * nl, s.H * nic, (size_t)p.Bo * nl, dbias1 + ((size_t)ob * s.N + p.n0w) * s.L, nl);
+          ++*launches;
+        }
+      }
+    }
+  }
+  if (!det) {
+    const size_t n = (size_t)s.B * s.L * HD;
+    const unsigned cg = (unsigned)std::min<size_t>((n / 8 + 255) / 256, 148 * 16);
+    auto convert = [&](const float* acc, void* out, float scale) {  // programmatic dependents of the main kernel
+      pdl_launch(s.swapped ? bk::dq_convert_kernel<T, true> : bk::dq_convert_kernel<T, false>, dim3(cg), dim3(256), 0,
+                 acc, (T*)out, n, scale, s.B, s.L, HD, s.flag);
+    };
+    convert(dqacc, dq, s.scale);
+    if (dkv_reduce) {  // dK = scale * dK_acc, dV = dV_acc
+      convert(dkacc, dk, s.scale);
+      convert(dvacc, dv, 1.f);
+    }
   }
   return EVO_OK;
 }

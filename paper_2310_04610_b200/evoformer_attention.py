@@ -19,6 +19,22 @@ from . import _native as N
 _DT = {torch.float32: N.EVO_F32, torch.bfloat16: N.EVO_BF16, torch.float16: N.EVO_F16}
 _PATHS = {"auto": N.EVO_PATH_AUTO, "simt": N.EVO_PATH_SIMT, "tcgen05": N.EVO_PATH_TCGEN05}
 
+# NumericError contract of the reference (attention_tiled.cpp:49-65, 125-127, 209): on by default —
+# the kernels flag NaN inputs / non-finite logit rows and each call waits for its stream to report
+# them. Off, the calls are fully asynchronous (what a training loop that trusts its inputs wants).
+_NUMERIC_CHECKS = True
+
+
+def set_numeric_checks(on: bool) -> bool:
+    """Default of `check_numerics` for every operator call; returns the previous setting."""
+    global _NUMERIC_CHECKS
+    prev, _NUMERIC_CHECKS = _NUMERIC_CHECKS, bool(on)
+    return prev
+
+
+def numeric_checks() -> bool:
+    return _NUMERIC_CHECKS
+
 
 def _as5d(x: torch.Tensor) -> torch.Tensor:
     if x.dim() == 4:
@@ -29,15 +45,19 @@ def _as5d(x: torch.Tensor) -> torch.Tensor:
 
 
 def make_desc(q: torch.Tensor, bias1, bias2, scale: Optional[float], path: str = "auto",
-              dbias_dtype: Optional[torch.dtype] = None) -> N.Desc:
+              dbias_dtype: Optional[torch.dtype] = None, check_numerics: Optional[bool] = None,
+              deterministic: bool = False) -> N.Desc:
     q5 = _as5d(q)
     Bo, Nr, L, H, D = q5.shape
     if q.dtype not in _DT:
         raise N.ValidationError(f"unsupported dtype {q.dtype}")
     s = 1.0 / math.sqrt(D) if scale is None else float(scale)
     dbt = _DT[dbias_dtype] if dbias_dtype is not None else N.EVO_F32
-    return N.Desc(Bo, Nr, L, H, D, _DT[q.dtype], s, int(bias1 is not None), int(bias2 is not None),
-                  dbt, _PATHS[path])
+    d = N.Desc(Bo, Nr, L, H, D, _DT[q.dtype], s, int(bias1 is not None), int(bias2 is not None),
+               dbt, _PATHS[path])
+    d.check_numerics = int(_NUMERIC_CHECKS if check_numerics is None else check_numerics)
+    d.deterministic = int(deterministic)
+    return d
 
 
 def _check_inputs(q, k, v, bias1, bias2):
@@ -65,12 +85,13 @@ def _stream():
     return torch.cuda.current_stream().cuda_stream
 
 
-def evoformer_attention_forward(q, k, v, bias1=None, bias2=None, scale=None, path: str = "auto"
-                                ) -> Tuple[torch.Tensor, torch.Tensor]:
-    """O = softmax(scale*QK^T + bias1 + bias2) V and LSE [B, H, L] (fp32, natural log)."""
+def evoformer_attention_forward(q, k, v, bias1=None, bias2=None, scale=None, path: str = "auto",
+                                check_numerics: Optional[bool] = None) -> Tuple[torch.Tensor, torch.Tensor]:
+    """O = softmax(scale*QK^T + bias1 + bias2) V and LSE [B, H, L] (fp32, natural log).
+    NumericError on NaN inputs / non-finite logit rows when numeric checks are on."""
     lib = N.load()
     _check_inputs(q, k, v, bias1, bias2)
-    d = make_desc(q, bias1, bias2, scale, path)
+    d = make_desc(q, bias1, bias2, scale, path, check_numerics=check_numerics)
     o = torch.empty_like(q)
     lse = torch.empty((d.Bo * d.N, d.H, d.L), device=q.device, dtype=torch.float32)
     wsb = lib.evo_attn_fwd_workspace_size(d)
@@ -84,18 +105,21 @@ def evoformer_attention_backward(dout, q, k, v, o, lse, bias1=None, bias2=None, 
                                  need_dbias1: bool = False, need_dbias2: bool = True,
                                  dbias_dtype: Optional[torch.dtype] = torch.float32,
                                  path: str = "auto", dbias_out: Optional[Tuple] = None,
-                                 dbias2_multicast: int = 0):
+                                 dbias2_multicast: int = 0, deterministic: bool = False,
+                                 check_numerics: Optional[bool] = None):
     """dQ, dK, dV and the broadcast-reduced bias gradients.
 
     dbias2 is sum over the N (row) axis of dS, reduced inside the kernels, in
     dbias_dtype (float32 = the reference's UpcastF32 policy). dbias_out lets a
     caller pass fp32 accumulators (dbias1, dbias2) that are ADDED to.
+    deterministic = AccumPolicy::deterministic (attention_tiled.hpp:35-44): every cross-CTA
+    reduction runs in a fixed order, two runs are bit-identical.
     """
     lib = N.load()
     _check_inputs(q, k, v, bias1, bias2)
     if dout.shape != q.shape or o.shape != q.shape or dout.dtype != q.dtype or o.dtype != q.dtype:
         raise N.ValidationError("output and grad_output must match Q/K/V shape and dtype")
-    d = make_desc(q, bias1, bias2, scale, path, dbias_dtype)
+    d = make_desc(q, bias1, bias2, scale, path, dbias_dtype, check_numerics, deterministic)
     d.dbias2_multicast = dbias2_multicast or None  # NVSwitch multicast address of a symmetric dBias2 buffer
     if tuple(lse.shape) != (d.Bo * d.N, d.H, d.L) or lse.dtype != torch.float32:
         raise N.ValidationError(f"lse must be [B, H, L] float32, got {tuple(lse.shape)} {lse.dtype}")
@@ -123,8 +147,12 @@ def last_launch_count() -> int:
     return int(N.load().evo_attn_last_launch_count())
 
 
-def resolved_path(q, bias1=None, bias2=None, path="auto") -> str:
-    r = N.load().evo_attn_resolved_path(make_desc(q, bias1, bias2, None, path))
+def resolved_path(q, bias1=None, bias2=None, path="auto", direction: str = "fwd") -> str:
+    """Kernel family a call resolves to: direction "fwd" or "bwd" (the tcgen05 backward's envelope is
+    narrower: 16-bit, D 16/32, L % 8 == 0)."""
+    d = make_desc(q, bias1, bias2, None, path)
+    lib = N.load()
+    r = (lib.evo_attn_resolved_path if direction == "fwd" else lib.evo_attn_resolved_bwd_path)(d)
     return {N.EVO_PATH_SIMT: "simt", N.EVO_PATH_TCGEN05: "tcgen05"}.get(r, "invalid")
 
 

@@ -65,9 +65,12 @@ def sharded_fwd_bwd(q, k, v, dout, bias1, bias2, group=None, dbias_dtype: torch.
         buf.zero_()
         handle.barrier(channel=0)  # every replica is zero before any rank adds
         try:
-            dq, dk, dv, db1, _ = bwd(dout, q, k, v, o, lse, bias1, bias2, need_dbias1=need1,
-                                     need_dbias2=True, dbias_dtype=torch.float32, dbias_out=(None, buf),
-                                     dbias2_multicast=handle.multicast_ptr)
+            # dbias_out holds fp32 accumulators the kernels ADD to: the mask-bias gradient (per row,
+            # rank-local) needs its own zeroed buffer on this path too
+            db1 = torch.zeros(bias1.shape, device=q.device, dtype=torch.float32) if need1 else None
+            dq, dk, dv, _, _ = bwd(dout, q, k, v, o, lse, bias1, bias2, need_dbias1=need1,
+                                   need_dbias2=True, dbias_dtype=torch.float32, dbias_out=(db1, buf),
+                                   dbias2_multicast=handle.multicast_ptr)
             handle.barrier(channel=0)  # every rank's adds have landed in every replica
             db2 = buf.view(bias2.shape).clone()
         except UnsupportedError:  # shape outside the tcgen05 backward: reduce with NCCL instead

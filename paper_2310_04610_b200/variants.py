@@ -33,7 +33,7 @@ import torch
 
 from . import _native as N
 from .evoformer_attention import (_DT, _PATHS, _ptr, _stream, EvoformerAttentionFunction,
-                                  evoformer_attention_forward)
+                                  evoformer_attention_forward, numeric_checks)
 
 
 class AttentionVariant(enum.Enum):
@@ -148,6 +148,7 @@ def _desc(q, B, L, H, D, mask, bias, swap, path="auto", dbias_dtype=None):
                int(bias is not None), _DT[dbias_dtype] if dbias_dtype is not None else N.EVO_F32,
                _PATHS[path])
     d.axes_swapped = int(swap)
+    d.check_numerics = int(numeric_checks())
     return d
 
 
