@@ -20,11 +20,14 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-I", os.path.join(ROOT, "include"),
          "--expt-relaxed-constexpr", "-Xptxas", "-warn-spills"] + os.environ.get("EVO_NVCC_EXTRA", "").split()
-SOURCES = ["evoattn_capi.cu", "tc_kernels.cu", "evoattn_inputs.cu"]
+# (source, extra flags): tc_kernels.cu compiles as three parallel translation units (forward,
+# backward D = 32, backward D = 16; see EVO_TU there)
+SOURCES = [("evoattn_capi.cu", []), ("evoattn_inputs.cu", []), ("tc_kernels.cu", ["-DEVO_TU=1"]),
+           ("tc_kernels.cu", ["-DEVO_TU=2"]), ("tc_kernels.cu", ["-DEVO_TU=3"])]
 
 
 def _sources():
-    return [s for s in SOURCES if os.path.exists(os.path.join(CSRC, s))]
+    return [(s, f) for s, f in SOURCES if os.path.exists(os.path.join(CSRC, s))]
 
 
 def _needs_rebuild() -> bool:
@@ -46,10 +49,10 @@ def build(force: bool = False, verbose: bool = False, out: str = LIB, extra=()) 
     objs = []
     cmds = []
     tag = os.path.basename(out).replace(".so", "")
-    for src in _sources():
-        obj = os.path.join(LIBDIR, f"{tag}_" + src.replace(".cu", ".o"))
+    for k, (src, sflags) in enumerate(_sources()):
+        obj = os.path.join(LIBDIR, f"{tag}_{k}_" + src.replace(".cu", ".o"))
         objs.append(obj)
-        cmds.append([NVCC, *ARCH, *FLAGS, *extra, "-c", os.path.join(CSRC, src), "-o", obj])
+        cmds.append([NVCC, *ARCH, *FLAGS, *sflags, *extra, "-c", os.path.join(CSRC, src), "-o", obj])
 
     def run(cmd):
         r = subprocess.run(cmd, capture_output=True, text=True)

@@ -57,6 +57,9 @@ constexpr uint32_t kDb1Col = 384;
 #ifndef EVO_BWD_LATE_PDS
 #define EVO_BWD_LATE_PDS 1  // softmax waits for its P/dS buffer only before the first store
 #endif
+#ifndef EVO_BWD_DS_TMEM
+#define EVO_BWD_DS_TMEM 0  // 1: dS also written (bf16) into TMEM over its S columns: dQ and the dBias2 strip become
+#endif                     // TS-MMAs (A from TMEM), 32 KB less shared-memory operand traffic per step
 #ifndef EVO_BWD_POLY
 #define EVO_BWD_POLY 0
 #endif
@@ -133,21 +136,28 @@ struct Walker {
     return e < t1 ? e : t1;
   }
 };
+// rows walked per unit: the launch's row window (deterministic mode) or all N rows
+template <bool SAFE>
+__device__ __forceinline__ int walk_rows(const Params& p) { return SAFE ? p.nw : p.N; }
+template <bool SAFE>
 __device__ __forceinline__ Walker make_walker(const Params& p) {
+  const int nw = walk_rows<SAFE>(p);
   if (p.aligned) {
     const long long unit = blockIdx.x / p.split, part = blockIdx.x % p.split;
-    const long long base = unit * p.nw;
-    return Walker{base + p.nw * part / p.split, base + p.nw * (part + 1) / p.split, p.nw};
+    const long long base = unit * nw;
+    return Walker{base + nw * part / p.split, base + nw * (part + 1) / p.split, nw};
   }
-  return Walker{p.total * blockIdx.x / gridDim.x, p.total * (blockIdx.x + 1) / gridDim.x, p.nw};
+  return Walker{p.total * blockIdx.x / gridDim.x, p.total * (blockIdx.x + 1) / gridDim.x, nw};
 }
 struct Unit {
   int ob, h, jt, ic, it0, it1, n0;  // query tiles [it0, it1) of chunk ic
 };
+template <bool SAFE>
 __device__ __forceinline__ Unit unit_of(long long s0, const Params& p) {
   Unit u;
-  long long x = s0 / p.nw;
-  u.n0 = (int)(s0 - x * p.nw);  // window-local row
+  const int nw = walk_rows<SAFE>(p);
+  long long x = s0 / nw;
+  u.n0 = (int)(s0 - x * nw);  // window-local row
   u.ic = (int)(x % p.nIC);
   x /= p.nIC;
   u.jt = (int)(x % p.nKT);
@@ -207,7 +217,9 @@ __device__ __forceinline__ void red_v4_multimem(float* mc_addr, float a, float b
                : "memory");
 }
 
-template <int D, bool F16, bool CH, bool SW>  // CH: the query axis is split into chunks (L > 384); SW: raw [L, B, H, D] layout
+// CH: the query axis is split into chunks (L > 384); SW: raw [L, B, H, D] layout; SAFE: the deterministic
+// and numeric-check code paths are compiled in (selected at run time by p.det / p.flag)
+template <int D, bool F16, bool CH, bool SW, bool SAFE>
 __global__ void __launch_bounds__(kThreads, 1)
     bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
                const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmdO,
@@ -253,7 +265,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   const int warp = threadIdx.x / 32;
   const int lane = threadIdx.x % 32;
-  const Walker W = make_walker(p);
+  const Walker W = make_walker<SAFE>(p);
   constexpr uint32_t kSw = ptx::swizzle_code(C::kRowBytes);
 
   if (threadIdx.x == 0) {
@@ -261,7 +273,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     for (int s = 0; s < C::kKStages; ++s) { ptx::mbar_init(&k_full[s], 1); ptx::mbar_init(&k_empty[s], 1); }
     for (int s = 0; s < 2; ++s) {
       ptx::mbar_init(&s_full[s], 1);
-      ptx::mbar_init(&s_free[s], kGroupThreads);   // buffer s serves the group of steps s (mod 2)
+      // buffer s serves the group of steps s (mod 2); with dS in TMEM it frees when the gradient MMAs
+      // reading dS from it completed, else when the softmax threads loaded S and dP
+      ptx::mbar_init(&s_free[s], EVO_BWD_DS_TMEM ? 1 : kGroupThreads);
       ptx::mbar_init(&pds_full[s], kGroupThreads);
       ptx::mbar_init(&pds_free[s], 1);
     }
@@ -317,7 +331,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       uint32_t bph = 0, pstep = 0;
       for (long long s0 = W.t0; s0 < W.t1; s0 = W.seg_end(s0)) {
         const int cnt = (int)(W.seg_end(s0) - s0);
-        const Unit u = unit_of(s0, p);
+        const Unit u = unit_of<SAFE>(s0, p);
         const int plane = u.ob * p.H + u.h;
         if (p.has_bias2) {
           ptx::mbar_wait(bias_empty, bph ^ 1);
@@ -328,7 +342,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         int n = u.n0;
         for (int a = 0; a < cnt; ++a, ++n) {
-          const int b = u.ob * p.N + p.n0w + n;
+          const int b = u.ob * p.N + (SAFE ? p.n0w : 0) + n;
           // K, V (and the bias1 chunk) of this row's key tile
           ptx::mbar_wait(&k_empty[ks], kph ^ 1);
           const int nk = min(kBN, p.L - u.jt * kBN);  // keys of this tile (multiple of 8)
@@ -378,7 +392,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint32_t step = 0, rows = 0;
     for (long long s0 = W.t0; s0 < W.t1; s0 = W.seg_end(s0)) {
       const int cnt = (int)(W.seg_end(s0) - s0);
-      const Unit u = unit_of(s0, p);
+      const Unit u = unit_of<SAFE>(s0, p);
       for (int a = 0; a < cnt; ++a) {
         for (int it = (CH ? u.it0 : 0); it < (CH ? u.it1 : p.nQT); ++it) {
           const uint32_t sb = step & 1, ph = (step >> 1) & 1;
@@ -400,9 +414,13 @@ __global__ void __launch_bounds__(kThreads, 1)
             trace(p, kTbGradsStart, step);
             // dQ first: the epilogue drains it while dK / dV run, so the next step's dQ never waits
 #pragma unroll
-            for (int kk = 0; kk < ((EVO_BWD_EXP & 2) ? 0 : kBN / 16); ++kk)  // dQ = dS K: K = 64 keys (+32 B in the dS rows)
-              ptx::mma_ss(tdQ, ptx::desc_make(dsK + kk * 2, kHiP), ptx::desc_make(kB + kk * kRow16, kHiMN), idQ,
-                          kk > 0);
+            for (int kk = 0; kk < ((EVO_BWD_EXP & 2) ? 0 : kBN / 16); ++kk) {  // dQ = dS K: K = 64 keys
+              if (EVO_BWD_DS_TMEM)  // A = dS block kk, bf16 in TMEM at S columns [16kk, 16kk + 8)
+                ptx::mma_ts(tdQ, tmem + sb * 128 + kk * 16, ptx::desc_make(kB + kk * kRow16, kHiMN), idQ, kk > 0);
+              else  // A = dS from shared memory (+32 B in the dS rows)
+                ptx::mma_ss(tdQ, ptx::desc_make(dsK + kk * 2, kHiP), ptx::desc_make(kB + kk * kRow16, kHiMN), idQ,
+                            kk > 0);
+            }
             ptx::tc_commit(dq_full);
 #pragma unroll
             for (int kk = 0; kk < ((EVO_BWD_EXP & 1) ? 0 : kBM / 16); ++kk) {  // K = 128 queries: 16 rows per step
@@ -421,11 +439,16 @@ __global__ void __launch_bounds__(kThreads, 1)
               // dS block kk (K-major, 16 keys) times a 16 x 16 identity; the unit's first row initialises
               const uint32_t st = tmem + kStripCol + (uint32_t)(it - (CH ? u.it0 : 0)) * 64;
 #pragma unroll
-              for (int kk = 0; kk < kBN / 16; ++kk)
-                ptx::mma_ss(st + kk * 16, ptx::desc_make(dsK + kk * 2, kHiP), bIdent, idStrip, a > 0 ? 1u : 0u);
+              for (int kk = 0; kk < kBN / 16; ++kk) {
+                if (EVO_BWD_DS_TMEM)
+                  ptx::mma_ts(st + kk * 16, tmem + sb * 128 + kk * 16, bIdent, idStrip, a > 0 ? 1u : 0u);
+                else
+                  ptx::mma_ss(st + kk * 16, ptx::desc_make(dsK + kk * 2, kHiP), bIdent, idStrip, a > 0 ? 1u : 0u);
+              }
               if (last && a == cnt - 1) ptx::tc_commit(strip_full);
             }
             ptx::tc_commit(&pds_free[sb]);
+            if (EVO_BWD_DS_TMEM) ptx::tc_commit(&s_free[sb]);  // dS (in the S/dP buffer) read
             ptx::tc_commit(&q_empty[qs]);  // S/dP of this step completed before P/dS existed
             if (last) {
               ptx::tc_commit(kv_done);
@@ -453,7 +476,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint32_t step = 0;
     for (long long s0 = W.t0; s0 < W.t1; s0 = W.seg_end(s0)) {
       const int cnt = (int)(W.seg_end(s0) - s0);
-      const Unit u = unit_of(s0, p);
+      const Unit u = unit_of<SAFE>(s0, p);
       for (int a = 0; a < cnt; ++a) {
         ptx::mbar_wait(&k_full[ks], kph);
         if (p.aug) {
@@ -529,7 +552,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint32_t step = 0, bph = 0, uph = 0;
     for (long long s0 = W.t0; s0 < W.t1; s0 = W.seg_end(s0)) {
       const int cnt = (int)(W.seg_end(s0) - s0);
-      const Unit u = unit_of(s0, p);
+      const Unit u = unit_of<SAFE>(s0, p);
       if (p.has_bias2) ptx::mbar_wait(bias_full, bph);
       for (int a = 0; a < cnt; ++a) {
         for (int it = (CH ? u.it0 : 0); it < (CH ? u.it1 : p.nQT); ++it) {
@@ -565,7 +588,7 @@ __global__ void __launch_bounds__(kThreads, 1)
               braw[1] = lds128(bt + ((uint32_t)((2 * kb + 1) << 4) ^ r7));
             }
             ptx::tmem_ld_wait();
-            if (cb == kGroups - 1) {
+            if (!EVO_BWD_DS_TMEM && cb == kGroups - 1) {
               ptx::tc_fence_before();
               ptx::mbar_arrive(&s_free[sb]);  // S/dP buffer may be recomputed
             }
@@ -591,6 +614,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 dk[k / 2] = F16 ? ptx::pack_f16(d.x, d.y) : ptx::pack_bf16(d.x, d.y);
               }
             }
+            if (EVO_BWD_DS_TMEM) ptx::tmem_st8(tmem + lane_off + sb * 128 + col, dk);  // dS over this block's S
             // P and dS -> shared (128B swizzle; chunks 2kb, 2kb+1 of row r). The buffer's previous
             // readers (the gradient MMAs of step - 2) are waited for only now: the first block's
             // loads and exponentials overlap their tail
@@ -601,6 +625,10 @@ __global__ void __launch_bounds__(kThreads, 1)
               sts128(pbase + off, make_uint4(pk[4 * c], pk[4 * c + 1], pk[4 * c + 2], pk[4 * c + 3]));
               sts128(dbase + off, make_uint4(dk[4 * c], dk[4 * c + 1], dk[4 * c + 2], dk[4 * c + 3]));
             }
+          }
+          if (EVO_BWD_DS_TMEM) {
+            ptx::tmem_st_wait();
+            ptx::tc_fence_before();
           }
           ptx::fence_proxy_async_smem();
           ptx::mbar_arrive(&pds_full[sb]);
@@ -616,7 +644,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         uph ^= 1;
         ptx::tc_fence_after();
         const long long unit = s0 / p.nw;
-        if (p.det) {  // the unit's CTAs flush in part order: wait for the lower parts' warpgroups
+        if (SAFE && p.det) {  // the unit's CTAs flush in part order: wait for the lower parts' warpgroups
           const int part = unit_part(p, unit);
           if (tid_wg == 0)
             while (ld_acquire(p.tickets + unit) < part * kSoftWG) __nanosleep(64);
@@ -643,7 +671,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
         }
       }
-      if (p.dbias2 && p.det) {  // this warpgroup's adds are performed before the next part may start
+      if (p.dbias2 && SAFE && p.det) {  // this warpgroup's adds are performed before the next part may start
         __threadfence();
         ptx::named_bar_sync(1 + wg, 128);
         if (tid_wg == 0) atomicAdd(p.tickets + s0 / p.nw, 1);
@@ -666,10 +694,10 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint32_t step = 0, rows = 0;
     for (long long s0 = W.t0; s0 < W.t1; s0 = W.seg_end(s0)) {
       const int cnt = (int)(W.seg_end(s0) - s0);
-      const Unit u = unit_of(s0, p);
+      const Unit u = unit_of<SAFE>(s0, p);
       int n = u.n0;
       for (int a = 0; a < cnt; ++a, ++n) {
-        const int b = u.ob * p.N + p.n0w + n;
+        const int b = u.ob * p.N + (SAFE ? p.n0w : 0) + n;
         const int wrow = u.ob * p.nw + n;  // row of the window (deterministic partial slots)
         const int Bw = p.Bo * p.nw;
         for (int it = (CH ? u.it0 : 0); it < (CH ? u.it1 : p.nQT); ++it) {
@@ -698,7 +726,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           ptx::fence_proxy_async_smem();
           ptx::named_bar_sync(kEpiBar, 128);
           if (tid_e == 0) {
-            if (p.det) ptx::tma_store_4d(&tmdQ, stg, 0, u.h, it * kBM, u.jt * Bw + wrow);  // key tile jt's slot
+            if (SAFE && p.det) ptx::tma_store_4d(&tmdQ, stg, 0, u.h, it * kBM, u.jt * Bw + wrow);  // key tile jt's slot
             else ptx::tma_reduce_add_4d(&tmdQ, stg, 0, u.h, it * kBM, b);
             ptx::bulk_commit();
             trace(p, kTbDqOut, step);
@@ -719,7 +747,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (p.dbias1 && lane < 16) {  // lanes 0-15 of quadrant q4 hold keys q4*16 + lane (M=64 layout)
           const int jj = u.jt * kBN + q4 * 16 + lane;
           if (jj < p.L) {
-            if (p.det) p.db1_part[(((size_t)u.h * p.nIC + u.ic) * Bw + wrow) * p.L + jj] = __uint_as_float(b1v[0]);
+            if (SAFE && p.det) p.db1_part[(((size_t)u.h * p.nIC + u.ic) * Bw + wrow) * p.L + jj] = __uint_as_float(b1v[0]);
             else atomicAdd(p.dbias1 + (size_t)b * p.L + jj, __uint_as_float(b1v[0]));
           }
         }
@@ -743,7 +771,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           ptx::fence_proxy_async_smem();
           ptx::named_bar_sync(kEpiBar, 128);
           if (tid_e == 0) {
-            if (p.det) {  // chunk ic's slot
+            if (SAFE && p.det) {  // chunk ic's slot
               ptx::tma_store_4d(&tmdK, stg, 0, u.h, u.jt * kBN, u.ic * Bw + wrow);
               ptx::tma_store_4d(&tmdV, stg + 64 * D, 0, u.h, u.jt * kBN, u.ic * Bw + wrow);
             } else {
@@ -757,7 +785,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         const int j = u.jt * kBN + krow;
         if (j < p.L) {
-          if (p.flag) {
+          if (SAFE && p.flag) {
             bool nan = false;
 #pragma unroll
             for (int d = 0; d < D; ++d) nan |= isnan(__uint_as_float(v[d]));
@@ -829,7 +857,7 @@ __global__ void prep_kernel(const T* __restrict__ dout, const T* __restrict__ o,
 }
 
 // lse2 / delta padded to whole 128-row tiles: lse2 = lse * log2e (+inf past L), delta (0 past L)
-__global__ void pad_rows_kernel(const float* __restrict__ lse, const float* __restrict__ delta, float* __restrict__ lse2,
+static __global__ void pad_rows_kernel(const float* __restrict__ lse, const float* __restrict__ delta, float* __restrict__ lse2,
                                 float* __restrict__ delta_p, int L, int Lp, long long rows, float4* __restrict__ zero,
                                 long long nzero4) {
   ptx::pdl_launch_dependents();

@@ -94,6 +94,11 @@ __device__ __forceinline__ float2 unpack2(uint32_t w) {  // two packed 16-bit fl
     return make_float2(__uint_as_float(w << 16), __uint_as_float(w & 0xFFFF0000u));
   }
 }
+__device__ __forceinline__ float fmax3(float a, float b, float c) {
+  float d;
+  asm("max.f32 %0, %1, %2, %3;" : "=f"(d) : "f"(a), "f"(b), "f"(c));
+  return d;
+}
 __device__ __forceinline__ uint4 lds128(uint32_t a) {
   uint4 v;
   asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(a));
@@ -143,7 +148,7 @@ __device__ __forceinline__ SegInfo seg_info(long long s0, const FwdParams& p) {
   return si;
 }
 
-template <int D, bool F16, int BM>
+template <int D, bool F16, int BM, bool SAFE>  // SAFE: numeric checks compiled in
 __global__ void __launch_bounds__(FwdCfg<D>::kThreads, 1)
     fwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
                const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmB2,
@@ -484,7 +489,11 @@ __global__ void __launch_bounds__(FwdCfg<D>::kThreads, 1)
           if (streamed) { slot = bslot; ptx::mbar_wait(&bias_full[slot], bph); }
           ptx::tmem_ld_wait();
           auto sv = [&](int k) { return __uint_as_float(k < 32 ? ra[k & 31] : rb[k & 31]); };
-          // ---- x = (S + bias1/scale) * scale * log2e + bias2 * log2e   (log2 domain)
+          // ---- x = (S + bias1/scale) * scale * log2e + bias2 * log2e - m   (log2 domain), relative to the
+          // running max m (0 before the first finite logit): one ffma2 per pair (bias path: two), and the
+          // exponent argument is final unless the max grows past the lazy-rescale threshold
+          const float base0 = m_run == -INFINITY ? 0.f : m_run;
+          const float2 nb0 = make_float2(-base0, -base0);
           float2 x[32];
           if constexpr (resident || streamed) {
             // 128B-swizzled bias tile: 8-key chunk c of row r sits at chunk c ^ (r & 7)
@@ -495,19 +504,19 @@ __global__ void __launch_bounds__(FwdCfg<D>::kThreads, 1)
               const uint32_t wv[4] = {raw.x, raw.y, raw.z, raw.w};
 #pragma unroll
               for (int e = 0; e < 4; ++e)
-                x[c * 4 + e] = __ffma2_rn(unpack2<F16>(wv[e]), lg2,
-                                          __fmul2_rn(make_float2(sv(c * 8 + 2 * e), sv(c * 8 + 2 * e + 1)), scl2));
+                x[c * 4 + e] = __ffma2_rn(make_float2(sv(c * 8 + 2 * e), sv(c * 8 + 2 * e + 1)), scl2,
+                                          __ffma2_rn(unpack2<F16>(wv[e]), lg2, nb0));
             }
           } else if constexpr (BM == kBiasGlobal) {
 #pragma unroll
             for (int k = 0; k < kBN; k += 2) {
               const int ja = min(j0 + k, p.L - 1), jb = min(j0 + k + 1, p.L - 1);
               const float2 bv = make_float2(load_half<F16>(b2row, ja), load_half<F16>(b2row, jb));
-              x[k / 2] = __ffma2_rn(make_float2(sv(k), sv(k + 1)), scl2, __fmul2_rn(bv, lg2));
+              x[k / 2] = __ffma2_rn(make_float2(sv(k), sv(k + 1)), scl2, __ffma2_rn(bv, lg2, nb0));
             }
           } else {
 #pragma unroll
-            for (int k = 0; k < kBN; k += 2) x[k / 2] = __fmul2_rn(make_float2(sv(k), sv(k + 1)), scl2);
+            for (int k = 0; k < kBN; k += 2) x[k / 2] = __ffma2_rn(make_float2(sv(k), sv(k + 1)), scl2, nb0);
           }
           // ---- bias release: streamed tiles per use; the resident block after the segment's last use
           if (streamed || (resident && last_row && j == p.nKT - 1)) {
@@ -524,13 +533,16 @@ __global__ void __launch_bounds__(FwdCfg<D>::kThreads, 1)
 #pragma unroll
           for (int k = 0; k < 4; ++k) mx[k] = fmaxf(x[k].x, x[k].y);
 #pragma unroll
-          for (int k = 4; k < 32; ++k) mx[k & 3] = fmaxf(mx[k & 3], fmaxf(x[k].x, x[k].y));
-          const float mt = fmaxf(fmaxf(mx[0], mx[1]), fmaxf(mx[2], mx[3]));
-          const bool grow = mt > m_run + kRescaleThreshold;  // also true for the first finite tile
+          for (int k = 4; k < 32; ++k) mx[k & 3] = fmax3(mx[k & 3], x[k].x, x[k].y);
+          const float mt = fmaxf(fmaxf(mx[0], mx[1]), fmaxf(mx[2], mx[3]));  // tile max minus base0
+          // grow: the first tile with a finite logit, or the max rose by more than the threshold
+          const bool grow = m_run == -INFINITY ? mt != -INFINITY : mt > kRescaleThreshold;
+          float dl = 0.f;  // re-bases the exponent arguments on a grown max (0 in the steady state)
           if (__any_sync(0xffffffffu, grow)) {
-            const float m_new = grow ? mt : m_run;
+            const float m_new = grow ? base0 + mt : m_run;
             const float alpha = ex2(m_run - (m_new == -INFINITY ? 0.f : m_new));  // 0 when m_run=-inf
             l_run *= alpha;
+            dl = grow ? mt : 0.f;
             if (j > 0) {
               // O holds the PVs of earlier tiles: wait for the last one, scale these rows in TMEM
               const uint32_t tp = tcount - 1;
@@ -548,13 +560,12 @@ __global__ void __launch_bounds__(FwdCfg<D>::kThreads, 1)
             }
             m_run = m_new;
           }
-          const float base = m_run == -INFINITY ? 0.f : m_run;
-          const float2 nb = make_float2(-base, -base);
           float2 sum[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
           uint32_t pk[32];
+          const float2 nd = make_float2(-dl, -dl);
 #pragma unroll
           for (int k = 0; k < 32; ++k) {
-            float2 t = __fadd2_rn(x[k], nb);
+            float2 t = __fadd2_rn(x[k], nd);
             if (kPolyEvery > 0 && k % kPolyEvery == kPolyEvery - 1) {
               t = ex2_poly2(t);  // every kPolyEvery-th pair on the FMA pipe, the rest on MUFU
             } else {
@@ -598,7 +609,7 @@ __global__ void __launch_bounds__(FwdCfg<D>::kThreads, 1)
           for (int v = 0; v < D / 8; ++v) dst[v] = make_uint4(ow[4 * v], ow[4 * v + 1], ow[4 * v + 2], ow[4 * v + 3]);
           const float lv = l_run > 0.f ? (m_run + __log2f(l_run)) * kLn2 : -INFINITY;
           p.lse[((size_t)b * p.H + si.h) * p.L + i] = lv;
-          if (p.flag) {  // NumericError: a NaN input or no finite logit in the row
+          if (SAFE && p.flag) {  // NumericError: a NaN input or no finite logit in the row
             bool nan = !isfinite(lv);
 #pragma unroll
             for (int d = 0; d < D; ++d) nan |= isnan(__uint_as_float(ov[d]));

@@ -8,16 +8,32 @@
 #include <cstring>
 #include <cstdlib>
 #include <mutex>
+#include <type_traits>
 
 #include "tc_bwd.cuh"
 #include "tc_fwd.cuh"
 #include "tc_kernels.cuh"
 
+// The file is compiled as three translation units in parallel (build.py): EVO_TU 1 = forward launch +
+// device queries, 2 = backward D = 32 (+ the backward entry points), 3 = backward D = 16. EVO_TU 0
+// (default) compiles everything into one unit.
+#ifndef EVO_TU
+#define EVO_TU 0
+#endif
+#define EVO_TU_FWD (EVO_TU == 0 || EVO_TU == 1)
+#define EVO_TU_BWD32 (EVO_TU == 0 || EVO_TU == 2)
+#define EVO_TU_BWD16 (EVO_TU == 0 || EVO_TU == 3)
+
 namespace evo {
 namespace tc {
 
+#if EVO_TU_FWD
 unsigned long long* g_trace = nullptr;
 unsigned long long* g_trace_bwd = nullptr;
+#else
+extern unsigned long long* g_trace;
+extern unsigned long long* g_trace_bwd;
+#endif
 
 namespace {
 
@@ -118,6 +134,7 @@ uint32_t aug_split(double c, bool f16) {
   return (uint32_t)hi | ((uint32_t)lo << 16);
 }
 
+#if EVO_TU_FWD
 template <int D, bool F16>
 evo_status launch_fwd(const evo_attn_desc* d, const Shape& s, const void* q, const void* k, const void* v,
                       void* o, float* lse, cudaStream_t st, int* launches, std::string* err) {
@@ -167,10 +184,14 @@ evo_status launch_fwd(const evo_attn_desc* d, const Shape& s, const void* q, con
     *err = "forward shared-memory budget exceeded (L too large)";
     return EVO_ERR_UNSUPPORTED;
   }
-  auto kern = p.bias_mode == kBiasResident   ? fwd_kernel<D, F16, kBiasResident>
-              : p.bias_mode == kBiasStreamed ? fwd_kernel<D, F16, kBiasStreamed>
-              : p.bias_mode == kBiasGlobal   ? fwd_kernel<D, F16, kBiasGlobal>
-                                             : fwd_kernel<D, F16, kBiasNone>;
+  auto pick = [&](auto safe) {
+    constexpr bool S = decltype(safe)::value;
+    return p.bias_mode == kBiasResident   ? fwd_kernel<D, F16, kBiasResident, S>
+           : p.bias_mode == kBiasStreamed ? fwd_kernel<D, F16, kBiasStreamed, S>
+           : p.bias_mode == kBiasGlobal   ? fwd_kernel<D, F16, kBiasGlobal, S>
+                                          : fwd_kernel<D, F16, kBiasNone, S>;
+  };
+  auto kern = p.flag ? pick(std::true_type{}) : pick(std::false_type{});
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   // Grid: one CTA per SM. If every (ob, h, q-tile) unit can get >= 4 CTAs, give each unit the same
   // number of CTAs with aligned row ranges (the q-tiles of a row then run concurrently and share
@@ -189,6 +210,8 @@ evo_status launch_fwd(const evo_attn_desc* d, const Shape& s, const void* q, con
   ++*launches;
   return EVO_OK;
 }
+
+#endif  // EVO_TU_FWD
 
 // ---------------------------------------------------------------------------------- backward
 constexpr int kBwdChunk = 3;  // query tiles per backward unit: its dBias2 strip (3 x 64 TMEM columns) fits
@@ -370,8 +393,12 @@ evo_status launch_bwd(const evo_attn_desc* d, const Shape& s, const void* dout, 
         (const T*)dout, (const T*)o, lse, lse2, delta_p, s.B, s.L, s.H, Lp, zero4, nzero4, s.flag);
   }
   ++*launches;
-  auto kern = s.swapped ? (dkv_reduce ? bk::bwd_kernel<D, F16, true, true> : bk::bwd_kernel<D, F16, false, true>)
-                        : (dkv_reduce ? bk::bwd_kernel<D, F16, true, false> : bk::bwd_kernel<D, F16, false, false>);
+  auto pick = [&](auto safe) {
+    constexpr bool S = decltype(safe)::value;
+    return s.swapped ? (dkv_reduce ? bk::bwd_kernel<D, F16, true, true, S> : bk::bwd_kernel<D, F16, false, true, S>)
+                     : (dkv_reduce ? bk::bwd_kernel<D, F16, true, false, S> : bk::bwd_kernel<D, F16, false, false, S>);
+  };
+  auto kern = (det || s.flag) ? pick(std::true_type{}) : pick(std::false_type{});
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   const int G = sm_count();
   auto pdl_launch = [&](auto fn, dim3 grid, dim3 block, size_t shm, auto... args) {
@@ -445,6 +472,19 @@ evo_status launch_bwd(const evo_attn_desc* d, const Shape& s, const void* dout, 
 
 }  // namespace
 
+#define EVO_BWD_ARGS                                                                                               \
+  const evo_attn_desc *d, const Shape &s, const void *dout, const void *q, const void *k, const void *v,           \
+      const void *o, const float *lse, const float *delta, void *dq, void *dk, void *dv, float *dbias1,             \
+      float *dbias2, void *scratch, cudaStream_t st, int *launches, std::string *err
+#define EVO_BWD_PASS d, s, dout, q, k, v, o, lse, delta, dq, dk, dv, dbias1, dbias2, scratch, st, launches, err
+evo_status launch_bwd16(EVO_BWD_ARGS);
+#if EVO_TU_BWD16
+evo_status launch_bwd16(EVO_BWD_ARGS) {
+  return d->dtype == EVO_F16 ? launch_bwd<16, true>(EVO_BWD_PASS) : launch_bwd<16, false>(EVO_BWD_PASS);
+}
+#endif
+
+#if EVO_TU_FWD
 bool device_supported() {
   static int ok = -1;
   if (ok < 0) {
@@ -461,6 +501,9 @@ bool device_supported() {
 }
 
 size_t fwd_scratch_bytes(const evo_attn_desc*) { return 0; }
+#endif
+
+#if EVO_TU_BWD32
 size_t bwd_scratch_bytes(const evo_attn_desc* d) { return bwd_scratch_layout(d).total; }
 
 // tcgen05 backward: 16-bit inputs, D in {16, 32}, L % 8 == 0 (16B-aligned rows for the bulk copies).
@@ -470,19 +513,16 @@ bool bwd_available(const evo_attn_desc* d) {
   return d->dtype != EVO_F32 && (d->D == 16 || d->D == 32) && d->L % 8 == 0 && device_supported();
 }
 
-evo_status bwd(const evo_attn_desc* d, const Shape& s, const void* dout, const void* q, const void* k, const void* v,
-               const void* o, const float* lse, const float* delta, void* dq, void* dk, void* dv, float* dbias1, float* dbias2,
-               void* scratch, cudaStream_t st, int* launches, std::string* err) {
-  const bool f16 = d->dtype == EVO_F16;
+evo_status bwd(EVO_BWD_ARGS) {
   switch (d->D) {
-    case 16: return f16 ? launch_bwd<16, true>(d, s, dout, q, k, v, o, lse, delta, dq, dk, dv, dbias1, dbias2, scratch, st, launches, err)
-                        : launch_bwd<16, false>(d, s, dout, q, k, v, o, lse, delta, dq, dk, dv, dbias1, dbias2, scratch, st, launches, err);
-    case 32: return f16 ? launch_bwd<32, true>(d, s, dout, q, k, v, o, lse, delta, dq, dk, dv, dbias1, dbias2, scratch, st, launches, err)
-                        : launch_bwd<32, false>(d, s, dout, q, k, v, o, lse, delta, dq, dk, dv, dbias1, dbias2, scratch, st, launches, err);
+    case 16: return launch_bwd16(EVO_BWD_PASS);
+    case 32: return d->dtype == EVO_F16 ? launch_bwd<32, true>(EVO_BWD_PASS) : launch_bwd<32, false>(EVO_BWD_PASS);
     default: *err = "tcgen05 backward supports D in {16, 32}"; return EVO_ERR_UNSUPPORTED;
   }
 }
+#endif  // EVO_TU_BWD32
 
+#if EVO_TU_FWD
 evo_status fwd(const evo_attn_desc* d, const Shape& s, const void* q, const void* k, const void* v, void* o,
                float* lse, void*, cudaStream_t st, int* launches, std::string* err) {
   const bool f16 = d->dtype == EVO_F16;
@@ -497,10 +537,14 @@ evo_status fwd(const evo_attn_desc* d, const Shape& s, const void* q, const void
   }
 }
 
+#endif  // EVO_TU_FWD
+
 }  // namespace tc
 }  // namespace evo
 
 // Bring-up aid (not part of include/evoattn.h): record a clock64 timeline of CTA 0 of the next
 // forward launches into a device buffer of 8 x 64 uint64 (null disables).
+#if EVO_TU_FWD
 extern "C" void evo_attn_debug_set_trace(void* dev_buf) { evo::tc::g_trace = (unsigned long long*)dev_buf; }
 extern "C" void evo_attn_debug_set_trace_bwd(void* dev_buf) { evo::tc::g_trace_bwd = (unsigned long long*)dev_buf; }
+#endif

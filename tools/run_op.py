@@ -20,7 +20,7 @@ ap.add_argument("--path", default="auto")
 a = ap.parse_args()
 cfg = bench.CONFIGS[a.config]
 dev = torch.device("cuda:0")
-q, k, v, do, b1, b2 = (t.to(dev) for t in bench.make_inputs(cfg, (0, cfg[1]), dev))
+q, k, v, do, b1, b2 = (t.to(dev) for t in bench.make_inputs(cfg, (0, cfg[1])))
 o, lse = E.evoformer_attention_forward(q, k, v, b1, b2, path=a.path)
 for _ in range(a.iters):
     if a.what in ("fwd", "both"):

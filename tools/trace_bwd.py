@@ -10,7 +10,7 @@ from paper_2310_04610_b200 import _native as N
 args = [a for a in sys.argv[1:] if not a.startswith("--")]
 cfg = bench.CONFIGS[args[0] if args else "c4"]
 dev = torch.device("cuda:0")
-q, k, v, do, b1, b2 = (t.to(dev) for t in bench.make_inputs(cfg, (0, cfg[1]), dev))
+q, k, v, do, b1, b2 = (t.to(dev) for t in bench.make_inputs(cfg, (0, cfg[1])))
 if "--nobias" in sys.argv:
     b1 = b2 = None
 if "--nob1" in sys.argv:

@@ -8,7 +8,7 @@ from paper_2310_04610_b200 import _native as N
 
 cfg = bench.CONFIGS[sys.argv[1] if len(sys.argv) > 1 else "c4"]
 dev = torch.device("cuda:0")
-q, k, v, do, b1, b2 = (t.to(dev) for t in bench.make_inputs(cfg, (0, cfg[1]), dev))
+q, k, v, do, b1, b2 = (t.to(dev) for t in bench.make_inputs(cfg, (0, cfg[1])))
 for _ in range(3):
     E.evoformer_attention_forward(q, k, v, b1, b2)
 buf = torch.zeros(12 * 64, dtype=torch.int64, device=dev)
