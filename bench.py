@@ -287,6 +287,9 @@ def main():
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
+        # the persistent kernels hold 144 of the 148 SMs: keep NCCL's all-reduce kernel on the rest so it
+        # overlaps them instead of displacing CTAs
+        os.environ.setdefault("NCCL_MAX_CTAS", "4")
         dist.init_process_group("nccl", device_id=dev)
     # Timed loops run asynchronously: the NumericError host round trip (a stream sync per call) is
     # off there; the checked mode is timed separately below and reported beside the headline.
@@ -303,8 +306,21 @@ def main():
     B_local = Bo * (hi - lo)
     B_total = Bo * Nr if args.scaling == "strong" else Bo * Nr * world
 
+    pending = []
+
     def step():
-        return sharded_fwd_bwd(q, k, v, do, b1, b2)
+        # multi-GPU: the dBias2 all-reduce of this step runs asynchronously (NCCL's stream) and overlaps
+        # the next step's forward; the previous step's reduction is waited for here, the last one before
+        # the closing event
+        r = sharded_fwd_bwd(q, k, v, do, b1, b2, async_reduce=world > 1)
+        while pending:
+            pending.pop().wait()
+        pending.append(r)
+        return r
+
+    def drain():
+        while pending:
+            pending.pop().wait()
 
     def barrier():
         if world > 1:
@@ -313,6 +329,7 @@ def main():
     # ---- warm-up + launch count
     for _ in range(args.warmup):
         step()
+    drain()
     torch.cuda.synchronize()
     E.evoformer_attention_forward(q, k, v, b1, b2)
     n_fwd = E.last_launch_count()
@@ -327,6 +344,7 @@ def main():
     base = torch.cuda.memory_allocated()
     torch.cuda.reset_peak_memory_stats()
     r = step()
+    drain()
     torch.cuda.synchronize()
     outs = sum(t.numel() * t.element_size() for t in (r.o, r.lse, r.dq, r.dk, r.dv) if t is not None)
     outs += sum(t.numel() * t.element_size() for t in (r.dbias1, r.dbias2) if t is not None)
@@ -342,6 +360,7 @@ def main():
         ev0.record(stream)
         for _ in range(args.steps):
             step()
+        drain()
         ev1.record(stream)
         torch.cuda.synchronize()
         barrier()
@@ -366,7 +385,7 @@ def main():
     # the same step with the reference's NumericError checks on (each call waits for its stream)
     E.set_numeric_checks(True)
     barrier()
-    ms_checked = time_call(step, max(5, args.steps // 4))
+    ms_checked = time_call(lambda: (step(), drain()), max(5, args.steps // 4))
     E.set_numeric_checks(False)
 
     # ---- per-call timing (forward call, backward call) on the launching stream; the dominant call's
@@ -412,6 +431,7 @@ def main():
     host_in = host
     dev_sets = [[torch.empty_like(t, device=dev) for t in host_in] for _ in range(2)]
     r = step()
+    drain()
     host_out = [torch.empty(t.shape, dtype=t.dtype, pin_memory=True) for t in (r.dq, r.dk, r.dv, r.dbias2)]
     h2d = sum(t.numel() * t.element_size() for t in host_in)
     d2h = sum(t.numel() * t.element_size() for t in host_out)
@@ -436,7 +456,7 @@ def main():
             if i + 1 < nsteps:
                 upload(1 - cur)
             stream.wait_event(ready[cur])
-            rr = sharded_fwd_bwd(*dev_sets[cur])
+            rr = sharded_fwd_bwd(*dev_sets[cur]).wait()
             free[cur].record(stream)
             done = torch.cuda.Event()
             done.record(stream)

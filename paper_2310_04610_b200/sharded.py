@@ -40,10 +40,21 @@ class ShardedStep:
     dv: torch.Tensor
     dbias1: Optional[torch.Tensor]
     dbias2: Optional[torch.Tensor]
+    pending: Optional[object] = None  # in-flight dBias2 all-reduce (async_reduce)
+    dbias_dtype: torch.dtype = torch.float32
+
+    def wait(self) -> "ShardedStep":
+        """Make the current stream wait for the in-flight dBias2 all-reduce; dbias2 is then final."""
+        if self.pending is not None:
+            self.pending.wait()
+            self.pending = None
+            if self.dbias2 is not None and self.dbias_dtype != torch.float32:
+                self.dbias2 = self.dbias2.to(self.dbias_dtype)
+        return self
 
 
 def sharded_fwd_bwd(q, k, v, dout, bias1, bias2, group=None, dbias_dtype: torch.dtype = torch.float32,
-                    need_dbias1: bool = False, ops=None) -> ShardedStep:
+                    need_dbias1: bool = False, ops=None, async_reduce: bool = False) -> ShardedStep:
     """Forward + backward on this rank's row shard, dBias2 all-reduced.
 
     q/k/v/dout/bias1 are this rank's rows ([Bo, n_local, L, H, D]); bias2 is the full pair bias.
@@ -51,7 +62,10 @@ def sharded_fwd_bwd(q, k, v, dout, bias1, bias2, group=None, dbias_dtype: torch.
     all-reduce over the group completes it. The mask-bias gradient is off by
     default (the MSA mask carries no gradient in OpenFold; the headline step produces dQ, dK, dV
     and dBias2). `ops` = (forward, backward) overrides the CUDA operators (used by the CPU
-    gloo tests to drive the same control flow with the oracle).
+    gloo tests to drive the same control flow with the oracle). async_reduce: the all-reduce is
+    issued without blocking the compute stream (NCCL runs it on its own stream, ordered after this
+    backward), so it overlaps whatever the caller launches next (the next layer's or step's
+    forward); call .wait() on the result before reading dbias2.
     """
     fwd, bwd = ops if ops is not None else (evoformer_attention_forward, evoformer_attention_backward)
     o, lse = fwd(q, k, v, bias1, bias2)
@@ -81,6 +95,11 @@ def sharded_fwd_bwd(q, k, v, dout, bias1, bias2, group=None, dbias_dtype: torch.
             dout, q, k, v, o, lse, bias1, bias2, need_dbias1=need1,
             need_dbias2=bias2 is not None, dbias_dtype=torch.float32)
         if db2 is not None and world > 1:
+            if async_reduce:
+                work = dist.all_reduce(db2, op=dist.ReduceOp.SUM, group=group, async_op=True)
+                if db1 is not None and dbias_dtype != torch.float32:
+                    db1 = db1.to(dbias_dtype)
+                return ShardedStep(o, lse, dq, dk, dv, db1, db2, pending=work, dbias_dtype=dbias_dtype)
             dist.all_reduce(db2, op=dist.ReduceOp.SUM, group=group)
     if db2 is not None and dbias_dtype != torch.float32:
         db2 = db2.to(dbias_dtype)

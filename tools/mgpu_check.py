@@ -1,5 +1,9 @@
-"""Multi-GPU check of the row-sharding launcher (torchrun, one rank per GPU):
-the in-kernel NVLS dBias2 reduction (multicast) against a local backward + NCCL all-reduce.
+"""Multi-GPU checks of the row-sharding launcher (torchrun, one rank per GPU, NCCL):
+  1. strong sharding of one problem (rows split over ranks): every rank's O / dQ / dK / dV rows are
+     bit-identical to the single-GPU run of the whole problem, and the all-reduced dBias2 equals the
+     single-GPU dBias2 up to fp32 summation order (blocking and asynchronous all-reduce);
+  2. the in-kernel NVLS dBias2 reduction (EVO_MULTICAST=1, multimem.red through an NVSwitch multicast
+     mapping) against the NCCL all-reduce, where symmetric memory with multicast is available.
 
   python -m torch.distributed.run --nproc-per-node 2 --master-addr 127.0.0.1 tools/mgpu_check.py
 """
@@ -7,7 +11,6 @@ import os
 import sys
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
-os.environ.setdefault("EVO_MULTICAST", "1")  # exercise the in-kernel NVLS reduction
 import torch
 import torch.distributed as dist
 
@@ -19,16 +22,40 @@ rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
 torch.cuda.set_device(int(os.environ["LOCAL_RANK"]))
 dev = torch.device("cuda", int(os.environ["LOCAL_RANK"]))
 dist.init_process_group("nccl", device_id=dev)
+E.set_numeric_checks(False)
 cfg = (1, 96, 384, 8, 32, "bf16", "check")
-q, k, v, do, b1, b2 = (t.to(dev) for t in bench.make_inputs(cfg, (0, 96)))
-mc = sharded._multicast_dbias2(b2, None)
-r = sharded.sharded_fwd_bwd(q, k, v, do, b1, b2)
+full = [t.to(dev) for t in bench.make_inputs(cfg, (0, 96))]
+lo, hi = sharded.shard_rows(96, world, rank)
+mine = [t[:, lo:hi].contiguous() for t in full[:5]] + [full[5]]
+ok = True
+
+# single-GPU reference of the whole problem (every rank computes it alone, no collective)
+q, k, v, do, b1, b2 = full
 o, lse = E.evoformer_attention_forward(q, k, v, b1, b2)
-_, _, _, _, ref = E.evoformer_attention_backward(do, q, k, v, o, lse, b1, b2)
-dist.all_reduce(ref)
-torch.cuda.synchronize()
-err = ((r.dbias2 - ref).abs().max() / ref.abs().max()).item()
-print(f"rank {rank}: multicast={'yes' if mc is not None else 'no'} dbias2 max rel diff vs NCCL all-reduce {err:.2e}",
-      flush=True)
-assert err < 1e-5, err
+dq, dk, dv, _, db2 = E.evoformer_attention_backward(do, q, k, v, o, lse, b1, b2)
+ref = sharded.ShardedStep(o, lse, dq, dk, dv, None, db2)
+for mode in ("blocking", "async"):
+    r = sharded.sharded_fwd_bwd(*mine, async_reduce=(mode == "async")).wait()
+    torch.cuda.synchronize()
+    rows_equal = all(torch.equal(getattr(r, n), getattr(ref, n)[:, lo:hi]) for n in ("o", "dq", "dk", "dv"))
+    err = ((r.dbias2 - ref.dbias2).abs().max() / ref.dbias2.abs().max()).item()
+    print(f"rank {rank} [{mode} NCCL]: rows {lo}..{hi - 1} bit-identical to the 1-GPU run: {rows_equal}; "
+          f"dBias2 max rel diff vs 1 GPU {err:.2e}", flush=True)
+    ok &= rows_equal and err < 1e-5
+
+# in-kernel multicast (NVLS) reduction vs NCCL
+os.environ["EVO_MULTICAST"] = "1"
+sharded._MC_ENABLED = True
+mc = sharded._multicast_dbias2(full[5], None)
+if mc is not None:
+    r = sharded.sharded_fwd_bwd(*mine)
+    torch.cuda.synchronize()
+    err = ((r.dbias2 - ref.dbias2).abs().max() / ref.dbias2.abs().max()).item()
+    print(f"rank {rank} [multicast NVLS]: dBias2 max rel diff vs 1 GPU {err:.2e}", flush=True)
+    ok &= err < 1e-5
+else:
+    print(f"rank {rank}: symmetric-memory multicast unavailable, NVLS path skipped", flush=True)
+dist.barrier()
 dist.destroy_process_group()
+print(f"rank {rank}: {'PASS' if ok else 'FAIL'}", flush=True)
+sys.exit(0 if ok else 1)
