@@ -259,6 +259,9 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=20,
                     help="end-to-end steps timed (pipeline fill and drain amortised over them)")
     ap.add_argument("--all-configs", action="store_true", help="also time c1..c5 and attach them")
+    ap.add_argument("--reduce", default="blocking", choices=["blocking", "async"],
+                    help="multi-GPU dBias2 all-reduce: blocking (after the backward, on the compute stream) or "
+                         "async (NCCL's stream, overlapping the next step's forward)")
     ap.add_argument("--scaling", default="strong", choices=["weak", "strong"],
                     help="strong: the config's rows split over ranks (headline); weak: each rank owns a "
                          "full config's rows")
@@ -287,10 +290,9 @@ def main():
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
-        # the persistent kernels hold 144 of the 148 SMs: keep NCCL's all-reduce kernel on the rest so it
-        # overlaps them instead of displacing CTAs
-        os.environ.setdefault("NCCL_MAX_CTAS", "4")
-        dist.init_process_group("nccl", device_id=dev)
+        import datetime
+
+        dist.init_process_group("nccl", device_id=dev, timeout=datetime.timedelta(seconds=120))
     # Timed loops run asynchronously: the NumericError host round trip (a stream sync per call) is
     # off there; the checked mode is timed separately below and reported beside the headline.
     E.set_numeric_checks(False)
@@ -312,7 +314,7 @@ def main():
         # multi-GPU: the dBias2 all-reduce of this step runs asynchronously (NCCL's stream) and overlaps
         # the next step's forward; the previous step's reduction is waited for here, the last one before
         # the closing event
-        r = sharded_fwd_bwd(q, k, v, do, b1, b2, async_reduce=world > 1)
+        r = sharded_fwd_bwd(q, k, v, do, b1, b2, async_reduce=world > 1 and args.reduce == "async")
         while pending:
             pending.pop().wait()
         pending.append(r)
@@ -387,6 +389,12 @@ def main():
     barrier()
     ms_checked = time_call(lambda: (step(), drain()), max(5, args.steps // 4))
     E.set_numeric_checks(False)
+
+    allreduce_us = None
+    if world > 1 and b2 is not None:  # the dBias2 all-reduce alone (fp32, H*L*L), blocking on the stream
+        buf = torch.zeros(b2.numel(), device=dev, dtype=torch.float32)
+        barrier()
+        allreduce_us = 1e3 * time_call(lambda: dist.all_reduce(buf), 20)
 
     # ---- per-call timing (forward call, backward call) on the launching stream; the dominant call's
     # roofline against the bound of the SURVEY §8(d) model (max of the FLOP and byte times)
@@ -560,10 +568,12 @@ def main():
                        "D": D, "biases": "mask bias1 [Bo,N,1,1,L] + pair bias2 [Bo,1,H,L,L]",
                        "rows_per_rank": B_local, "rows_total": B_total,
                        "parallelism": f"rows_sharded_dp{world}", "kernel_path": path, "bwd_kernel_path": bwd_path,
+                       "dbias2_allreduce": args.reduce if world > 1 else None,
                        "numeric_checks": "off in the timed loop (ms_per_step_checked: on)",
                        "l2": "inputs+outputs larger than L2 (no flush needed)"
                        if ideal_bytes(B_local, L, H, D, elem) > 126e6 else "working set smaller than L2 (not flushed)"},
             "ms_per_step_checked": ms_checked,
+            "dbias2_allreduce_us": allreduce_us,
             "peak_mem": {"extra_bytes_per_rank": int(peak_extra), "naive_logits_bytes": naive,
                          "o_l_plan_bytes": 8 * B_local * H * L + 4 * H * L * L,
                          # the reference attn-bench column (run.cpp:223-234): naive / tiled peak

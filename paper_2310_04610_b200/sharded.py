@@ -54,7 +54,8 @@ class ShardedStep:
 
 
 def sharded_fwd_bwd(q, k, v, dout, bias1, bias2, group=None, dbias_dtype: torch.dtype = torch.float32,
-                    need_dbias1: bool = False, ops=None, async_reduce: bool = False) -> ShardedStep:
+                    need_dbias1: bool = False, ops=None, async_reduce: bool = False,
+                    deterministic: bool = False) -> ShardedStep:
     """Forward + backward on this rank's row shard, dBias2 all-reduced.
 
     q/k/v/dout/bias1 are this rank's rows ([Bo, n_local, L, H, D]); bias2 is the full pair bias.
@@ -91,9 +92,10 @@ def sharded_fwd_bwd(q, k, v, dout, bias1, bias2, group=None, dbias_dtype: torch.
             handle.barrier(channel=0)
             mc = None
     if mc is None:
+        kw = {"deterministic": True} if deterministic else {}
         dq, dk, dv, db1, db2 = bwd(
             dout, q, k, v, o, lse, bias1, bias2, need_dbias1=need1,
-            need_dbias2=bias2 is not None, dbias_dtype=torch.float32)
+            need_dbias2=bias2 is not None, dbias_dtype=torch.float32, **kw)
         if db2 is not None and world > 1:
             if async_reduce:
                 work = dist.all_reduce(db2, op=dist.ReduceOp.SUM, group=group, async_op=True)
