@@ -259,7 +259,7 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=20,
                     help="end-to-end steps timed (pipeline fill and drain amortised over them)")
     ap.add_argument("--all-configs", action="store_true", help="also time c1..c5 and attach them")
-    ap.add_argument("--reduce", default="blocking", choices=["blocking", "async"],
+    ap.add_argument("--reduce", default="async", choices=["blocking", "async"],
                     help="multi-GPU dBias2 all-reduce: blocking (after the backward, on the compute stream) or "
                          "async (NCCL's stream, overlapping the next step's forward)")
     ap.add_argument("--scaling", default="strong", choices=["weak", "strong"],
