@@ -314,10 +314,12 @@ def main():
         # multi-GPU: the dBias2 all-reduce of this step runs asynchronously (NCCL's stream) and overlaps
         # the next step's forward; the previous step's reduction is waited for here, the last one before
         # the closing event
-        r = sharded_fwd_bwd(q, k, v, do, b1, b2, async_reduce=world > 1 and args.reduce == "async")
+        async_reduce = world > 1 and args.reduce == "async"
+        r = sharded_fwd_bwd(q, k, v, do, b1, b2, async_reduce=async_reduce)
         while pending:
             pending.pop().wait()
-        pending.append(r)
+        if async_reduce:
+            pending.append(r)
         return r
 
     def drain():
@@ -360,9 +362,11 @@ def main():
         barrier()
         torch.cuda.synchronize()
         ev0.record(stream)
+        t_host = time.perf_counter()
         for _ in range(args.steps):
             step()
         drain()
+        t_host = time.perf_counter() - t_host
         ev1.record(stream)
         torch.cuda.synchronize()
         barrier()
@@ -375,6 +379,8 @@ def main():
     value = total_flops / (ms * 1e-3) / 1e12
 
     def time_call(fn, n):
+        for _ in range(2):  # warm (allocator, first-launch setup)
+            fn()
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         torch.cuda.synchronize()
         a.record(stream)
@@ -389,6 +395,14 @@ def main():
     barrier()
     ms_checked = time_call(lambda: (step(), drain()), max(5, args.steps // 4))
     E.set_numeric_checks(False)
+
+    # the same step with OpenFold's sigmoid output gate fused: gated forward + backward
+    gate = torch.empty_like(q).uniform_(-3, 3)
+    og, lse_g = E.evoformer_attention_forward_gated(q, k, v, gate, b1, b2)
+    gated_ms = time_call(lambda: (E.evoformer_attention_forward_gated(q, k, v, gate, b1, b2),
+                                  E.evoformer_attention_backward_gated(do, q, k, v, gate, og, lse_g, b1, b2)),
+                         max(10, args.steps // 4))
+    del gate, og, lse_g
 
     allreduce_us = None
     if world > 1 and b2 is not None:  # the dBias2 all-reduce alone (fp32, H*L*L), blocking on the stream
@@ -573,7 +587,10 @@ def main():
                        "l2": "inputs+outputs larger than L2 (no flush needed)"
                        if ideal_bytes(B_local, L, H, D, elem) > 126e6 else "working set smaller than L2 (not flushed)"},
             "ms_per_step_checked": ms_checked,
+            "host_enqueue_ms_per_step": t_host * 1e3 / args.steps,
             "dbias2_allreduce_us": allreduce_us,
+            "gated": {"ms_per_step": gated_ms, "tflops": flops(B_local, L, H, D) / gated_ms / 1e9,
+                      "what": "fwd+bwd with the fused sigmoid output gate (this rank's rows, no all-reduce)"},
             "peak_mem": {"extra_bytes_per_rank": int(peak_extra), "naive_logits_bytes": naive,
                          "o_l_plan_bytes": 8 * B_local * H * L + 4 * H * L * L,
                          # the reference attn-bench column (run.cpp:223-234): naive / tiled peak

@@ -92,6 +92,9 @@ typedef struct {
                              the chunked dK/dV) runs in a fixed order, so two runs are bit-identical
                              (SPEC.md:211). The SIMT backward is always ordered. 0 = unordered fp32
                              reductions (faster). */
+  int has_gate;           /* OpenFold's sigmoid output gate fused into the operator (the _gated entry
+                             points): o = sigmoid(G) * attention(q, k, v). Not in the reference
+                             (SPEC.md:153 lists gating as a non-goal); SURVEY.md §8(f)3. */
 } evo_attn_desc;
 
 size_t evo_attn_fwd_workspace_size(const evo_attn_desc* desc);
@@ -113,6 +116,21 @@ evo_status evo_attn_bwd(const evo_attn_desc* desc, const void* dout, const void*
                         const float* lse, void* dq, void* dk, void* dv, void* dbias1,
                         void* dbias2, int accumulate_dbias, void* workspace,
                         size_t workspace_bytes, evo_stream_t stream);
+
+/* Fused output gate (desc.has_gate = 1; OpenFold gating). gate = G logits and
+ * dgate in the layout of q / o. Forward: o = sigmoid(G) * softmax(...) v — the gate is applied in
+ * the forward kernel's epilogue, so the ungated output is never stored. Backward: dout is the
+ * gradient of the GATED output o (as the forward returned it); the preamble forms
+ * dO = dout * sigmoid(G) for the attention backward and dgate = dout * o * (1 - sigmoid(G)) in the same
+ * pass that computes delta = sum_d dout * o (the gate cancels in delta). */
+evo_status evo_attn_fwd_gated(const evo_attn_desc* desc, const void* q, const void* k, const void* v,
+                              const void* bias1, const void* bias2, const void* gate, void* o,
+                              float* lse, void* workspace, size_t workspace_bytes, evo_stream_t stream);
+evo_status evo_attn_bwd_gated(const evo_attn_desc* desc, const void* dout, const void* q, const void* k,
+                              const void* v, const void* bias1, const void* bias2, const void* gate,
+                              const void* o, const float* lse, void* dq, void* dk, void* dv, void* dgate,
+                              void* dbias1, void* dbias2, int accumulate_dbias, void* workspace,
+                              size_t workspace_bytes, evo_stream_t stream);
 
 /* Which kernel family AUTO resolves to for this descriptor (EVO_PATH_SIMT or
  * EVO_PATH_TCGEN05); negative if the descriptor is invalid. */

@@ -8,7 +8,8 @@ the C-ABI in include/evoattn.h. See DESIGN.md.
 from ._native import (CudaError, EvoAttnError, NumericError, UnsupportedError, UsageError,
                       ValidationError)
 from .evoformer_attention import (DS4Sci_EvoformerAttention, EvoformerAttentionFunction,
-                                  evoformer_attention_backward, evoformer_attention_forward,
+                                  evoformer_attention_backward, evoformer_attention_backward_gated,
+                                  evoformer_attention_forward, evoformer_attention_forward_gated,
                                   last_launch_count, numeric_checks, resolved_path, set_numeric_checks)
 from .variants import (AttentionVariant, chunked_forward, layout_from_msa, variant_attention, variant_forward,
                        variant_from_name)
@@ -19,4 +20,5 @@ __all__ = [
     "ValidationError", "NumericError", "UsageError", "CudaError", "UnsupportedError",
     "AttentionVariant", "variant_attention", "variant_from_name", "layout_from_msa",
     "chunked_forward", "variant_forward", "set_numeric_checks", "numeric_checks",
+    "evoformer_attention_forward_gated", "evoformer_attention_backward_gated",
 ]

@@ -18,7 +18,7 @@ EVO_PATH_AUTO, EVO_PATH_SIMT, EVO_PATH_TCGEN05 = 0, 1, 2
 EXPORTED = (
     "evo_attn_fwd_workspace_size", "evo_attn_bwd_workspace_size", "evo_attn_fwd", "evo_attn_bwd",
     "evo_attn_resolved_path", "evo_attn_resolved_bwd_path", "evo_attn_last_launch_count", "evo_attn_last_error",
-    "evo_attn_version", "evo_random_uniform", "evo_random_mask",
+    "evo_attn_version", "evo_random_uniform", "evo_random_mask", "evo_attn_fwd_gated", "evo_attn_bwd_gated",
 )
 
 
@@ -27,7 +27,8 @@ class Desc(C.Structure):
                 ("D", C.c_int64), ("dtype", C.c_int), ("scale", C.c_double),
                 ("has_bias1", C.c_int), ("has_bias2", C.c_int), ("dbias_dtype", C.c_int),
                 ("path", C.c_int), ("dbias2_multicast", C.c_void_p), ("need_dbias1", C.c_int),
-                ("axes_swapped", C.c_int), ("check_numerics", C.c_int), ("deterministic", C.c_int)]
+                ("axes_swapped", C.c_int), ("check_numerics", C.c_int), ("deterministic", C.c_int),
+                ("has_gate", C.c_int)]
 
 
 _lib = None
@@ -65,6 +66,12 @@ def load(build_if_missing: bool = True):
     lib.evo_attn_last_launch_count.restype = C.c_int
     lib.evo_attn_last_error.restype = C.c_char_p
     lib.evo_attn_version.restype = C.c_char_p
+    if hasattr(lib, "evo_attn_fwd_gated"):
+        lib.evo_attn_fwd_gated.argtypes = [dp, vp, vp, vp, vp, vp, vp, vp, vp, vp, sz, vp]
+        lib.evo_attn_fwd_gated.restype = C.c_int
+        lib.evo_attn_bwd_gated.argtypes = [dp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, C.c_int,
+                                           vp, sz, vp]
+        lib.evo_attn_bwd_gated.restype = C.c_int
     if not hasattr(lib, "evo_random_uniform"):  # an older A/B variant (tools/ab_time.py)
         _lib = lib
         return lib

@@ -73,7 +73,13 @@ struct Shape {
   const void* bias2;  // (Bo, H, L, L) or null
   int swapped;        // 1: q/k/v/o are (L, B, H, D) — the raw msa_col / tri_end layout (Bo == 1)
   int* flag;          // numeric-check word (NaN / non-finite results set it), or null: no checks
+  const void* gate;   // output-gate logits G, same layout as O (OpenFold gating: O_g = sigmoid(G) * O), or null
+  void* dgate;        // backward with a gate: dG output (layout of O)
+  void* dog;          // backward with a gate: workspace for the gated dO = dO_g * sigmoid(G)
 };
+
+// sigmoid on the MUFU pipe: 1 / (1 + 2^(-g log2 e)) (0 and 1 at the saturated ends)
+__device__ __forceinline__ float sigmoidf_fast(float g) { return __frcp_rn(1.f + ex2(-g * kLog2e)); }
 
 // NumericError detection (attention_tiled.cpp:49-53, 62-65, 125-127, 209): a NaN input or a
 // non-finite logit row shows up as a non-finite LSE / delta or a NaN output; the kernels OR a flag

@@ -35,6 +35,7 @@ evo_status validate(const evo_attn_desc* d) {
   if (d->dbias_dtype != EVO_F32 && d->dbias_dtype != d->dtype)
     return fail(EVO_ERR_VALIDATION, "dbias_dtype must be EVO_F32 or equal to dtype");
   if (!std::isfinite(d->scale)) return fail(EVO_ERR_NUMERIC, "attention scale must be finite");
+  if (d->has_gate != 0 && d->has_gate != 1) return fail(EVO_ERR_VALIDATION, "has_gate must be 0 or 1");
   if (d->axes_swapped != 0 && d->axes_swapped != 1)
     return fail(EVO_ERR_VALIDATION, "axes_swapped must be 0 or 1");
   if (d->axes_swapped && d->Bo != 1)
@@ -75,6 +76,9 @@ evo::Shape make_shape(const evo_attn_desc* d, const void* b1, const void* b2, in
   s.bias2 = b2;
   s.swapped = d->axes_swapped;
   s.flag = d->check_numerics ? flag : nullptr;
+  s.gate = nullptr;
+  s.dgate = nullptr;
+  s.dog = nullptr;
   return s;
 }
 
@@ -91,10 +95,11 @@ int64_t simt_batch_rows(const evo_attn_desc* d) {
 }
 
 // Bwd workspace layout: [header][delta B*H*L f32][dbias2 acc Bo*H*L*L f32][dbias1 acc B*L f32]
-// [SIMT partial planes of one row batch][tc scratch]
+// [gated dO, has_gate][SIMT partial planes of one row batch][tc scratch]
 struct BwdWs {
-  size_t delta, db2, db1, db2p, db1p, tc, total;
+  size_t delta, db2, db1, dog, db2p, db1p, tc, total;
 };
+size_t elem_bytes(const evo_attn_desc* d) { return d->dtype == EVO_F32 ? 4 : 2; }
 
 // Workspace sizing follows the kernels the call will run on the target device (sm_100a); on a host
 // without one (sizing only) the tcgen05 envelope is assumed.
@@ -114,6 +119,8 @@ BwdWs bwd_layout(const evo_attn_desc* d) {
   if (d->has_bias2) off += align_up((size_t)d->Bo * d->H * d->L * d->L * 4);
   w.db1 = off;
   if (d->has_bias1 && d->need_dbias1) off += align_up(B * d->L * 4);
+  w.dog = off;
+  if (d->has_gate) off += align_up(B * d->L * d->H * d->D * elem_bytes(d));
   w.db2p = w.db1p = w.tc = off;
   if (simt_bwd_path(d)) {
     const size_t nb = (size_t)simt_batch_rows(d);
@@ -264,13 +271,10 @@ size_t evo_attn_bwd_workspace_size(const evo_attn_desc* d) {
   return bwd_layout(d).total;
 }
 
-evo_status evo_attn_fwd(const evo_attn_desc* d, const void* q, const void* k, const void* v,
-                        const void* bias1, const void* bias2, void* o, float* lse,
-                        void* workspace, size_t workspace_bytes, evo_stream_t stream) {
-  g_launches = 0;
-  g_err.clear();
-  evo_status st = validate(d);
-  if (st) return st;
+static evo_status fwd_impl(const evo_attn_desc* d, const void* q, const void* k, const void* v,
+                           const void* bias1, const void* bias2, const void* gate, void* o, float* lse,
+                           void* workspace, size_t workspace_bytes, evo_stream_t stream) {
+  evo_status st = EVO_OK;
   if (!q || !k || !v || !o || !lse) return fail(EVO_ERR_VALIDATION, "q, k, v, o, lse must be non-null");
   if (d->has_bias1 != (bias1 != nullptr)) return fail(EVO_ERR_VALIDATION, "bias1 presence does not match the descriptor");
   if (d->has_bias2 != (bias2 != nullptr)) return fail(EVO_ERR_VALIDATION, "bias2 presence does not match the descriptor");
@@ -280,7 +284,8 @@ evo_status evo_attn_fwd(const evo_attn_desc* d, const void* q, const void* k, co
   cudaStream_t cs = (cudaStream_t)stream;
   int* flag = (int*)workspace;
   if ((st = numeric_begin(d, flag, cs))) return st;
-  const evo::Shape s = make_shape(d, bias1, bias2, flag);
+  evo::Shape s = make_shape(d, bias1, bias2, flag);
+  s.gate = gate;
   if (path == EVO_PATH_TCGEN05) {
     st = evo::tc::fwd(d, s, q, k, v, o, lse, (char*)workspace + kHeader, cs, &g_launches, &g_err);
     if (st) return st;
@@ -295,15 +300,34 @@ evo_status evo_attn_fwd(const evo_attn_desc* d, const void* q, const void* k, co
   return numeric_end(d, flag, cs, "attention logits are not finite or an input contains NaN (Q, K, V, bias)");
 }
 
-evo_status evo_attn_bwd(const evo_attn_desc* d, const void* dout, const void* q, const void* k,
-                        const void* v, const void* bias1, const void* bias2, const void* o,
-                        const float* lse, void* dq, void* dk, void* dv, void* dbias1,
-                        void* dbias2, int accumulate_dbias, void* workspace,
-                        size_t workspace_bytes, evo_stream_t stream) {
+evo_status evo_attn_fwd(const evo_attn_desc* d, const void* q, const void* k, const void* v,
+                        const void* bias1, const void* bias2, void* o, float* lse,
+                        void* workspace, size_t workspace_bytes, evo_stream_t stream) {
   g_launches = 0;
   g_err.clear();
   evo_status st = validate(d);
   if (st) return st;
+  if (d->has_gate) return fail(EVO_ERR_VALIDATION, "desc.has_gate: use evo_attn_fwd_gated");
+  return fwd_impl(d, q, k, v, bias1, bias2, nullptr, o, lse, workspace, workspace_bytes, stream);
+}
+
+evo_status evo_attn_fwd_gated(const evo_attn_desc* d, const void* q, const void* k, const void* v,
+                              const void* bias1, const void* bias2, const void* gate, void* o, float* lse,
+                              void* workspace, size_t workspace_bytes, evo_stream_t stream) {
+  g_launches = 0;
+  g_err.clear();
+  evo_status st = validate(d);
+  if (st) return st;
+  if (!d->has_gate || !gate) return fail(EVO_ERR_VALIDATION, "the gated forward needs desc.has_gate and a gate tensor");
+  return fwd_impl(d, q, k, v, bias1, bias2, gate, o, lse, workspace, workspace_bytes, stream);
+}
+
+static evo_status bwd_impl(const evo_attn_desc* d, const void* dout, const void* q, const void* k,
+                           const void* v, const void* bias1, const void* bias2, const void* gate, const void* o,
+                           const float* lse, void* dq, void* dk, void* dv, void* dgate, void* dbias1,
+                           void* dbias2, int accumulate_dbias, void* workspace, size_t workspace_bytes,
+                           evo_stream_t stream) {
+  evo_status st = EVO_OK;
   if (!dout || !q || !k || !v || !o || !lse || !dq || !dk || !dv)
     return fail(EVO_ERR_VALIDATION, "dout, q, k, v, o, lse, dq, dk, dv must be non-null");
   if (d->has_bias1 != (bias1 != nullptr)) return fail(EVO_ERR_VALIDATION, "bias1 presence does not match the descriptor");
@@ -332,7 +356,10 @@ evo_status evo_attn_bwd(const evo_attn_desc* d, const void* dout, const void* q,
   char* ws = (char*)workspace;
   int* flag = (int*)ws;
   if ((st = numeric_begin(d, flag, cs))) return st;
-  const evo::Shape s = make_shape(d, bias1, bias2, flag);
+  evo::Shape s = make_shape(d, bias1, bias2, flag);
+  s.gate = gate;
+  s.dgate = dgate;
+  s.dog = gate ? ws + w.dog : nullptr;
   float* delta = (float*)(ws + w.delta);
   // fp32 reduction targets: the caller's buffer when it is fp32, else workspace.
   const bool direct = d->dbias_dtype == EVO_F32;
@@ -348,10 +375,31 @@ evo_status evo_attn_bwd(const evo_attn_desc* d, const void* dout, const void* q,
     st = evo::tc::bwd(d, s, dout, q, k, v, o, lse, nullptr, dq, dk, dv, db1, db2, ws + w.tc, cs,
                       &g_launches, &g_err);
   } else {
-    switch (d->dtype) {
+    switch (d->dtype) {  // delta = sum dout * o (with a gate: the gated output and its gradient)
       case EVO_F32: launch_delta<float>(s, dout, o, delta, cs); break;
       case EVO_BF16: launch_delta<__nv_bfloat16>(s, dout, o, delta, cs); break;
       default: launch_delta<__half>(s, dout, o, delta, cs); break;
+    }
+    if (gate) {  // gate backward: the attention kernels take dO = dout * sigmoid(G); dG written
+      const size_t n = (size_t)s.B * s.L * s.H * s.D;
+      const int blocks = (int)std::min<size_t>((n + 255) / 256, 148 * 16);
+      switch (d->dtype) {
+        case EVO_F32:
+          evo::simt::gate_bwd_kernel<float><<<blocks, 256, 0, cs>>>(n, (const float*)dout, (const float*)o,
+                                                                    (const float*)gate, (float*)s.dog, (float*)dgate);
+          break;
+        case EVO_BF16:
+          evo::simt::gate_bwd_kernel<__nv_bfloat16><<<blocks, 256, 0, cs>>>(
+              n, (const __nv_bfloat16*)dout, (const __nv_bfloat16*)o, (const __nv_bfloat16*)gate,
+              (__nv_bfloat16*)s.dog, (__nv_bfloat16*)dgate);
+          break;
+        default:
+          evo::simt::gate_bwd_kernel<__half><<<blocks, 256, 0, cs>>>(n, (const __half*)dout, (const __half*)o,
+                                                                     (const __half*)gate, (__half*)s.dog, (__half*)dgate);
+          break;
+      }
+      ++g_launches;
+      dout = s.dog;
     }
     float* db1p = (float*)(ws + w.db1p);
     float* db2p = (float*)(ws + w.db2p);
@@ -378,6 +426,35 @@ evo_status evo_attn_bwd(const evo_attn_desc* d, const void* dout, const void* q,
     }
   }
   return numeric_end(d, flag, cs, "dO or the recomputed gradients contain NaN / non-finite values");
+}
+
+evo_status evo_attn_bwd(const evo_attn_desc* d, const void* dout, const void* q, const void* k,
+                        const void* v, const void* bias1, const void* bias2, const void* o,
+                        const float* lse, void* dq, void* dk, void* dv, void* dbias1,
+                        void* dbias2, int accumulate_dbias, void* workspace,
+                        size_t workspace_bytes, evo_stream_t stream) {
+  g_launches = 0;
+  g_err.clear();
+  evo_status st = validate(d);
+  if (st) return st;
+  if (d->has_gate) return fail(EVO_ERR_VALIDATION, "desc.has_gate: use evo_attn_bwd_gated");
+  return bwd_impl(d, dout, q, k, v, bias1, bias2, nullptr, o, lse, dq, dk, dv, nullptr, dbias1, dbias2,
+                  accumulate_dbias, workspace, workspace_bytes, stream);
+}
+
+evo_status evo_attn_bwd_gated(const evo_attn_desc* d, const void* dout, const void* q, const void* k,
+                              const void* v, const void* bias1, const void* bias2, const void* gate,
+                              const void* o, const float* lse, void* dq, void* dk, void* dv, void* dgate,
+                              void* dbias1, void* dbias2, int accumulate_dbias, void* workspace,
+                              size_t workspace_bytes, evo_stream_t stream) {
+  g_launches = 0;
+  g_err.clear();
+  evo_status st = validate(d);
+  if (st) return st;
+  if (!d->has_gate || !gate || !dgate)
+    return fail(EVO_ERR_VALIDATION, "the gated backward needs desc.has_gate, the gate and a dgate buffer");
+  return bwd_impl(d, dout, q, k, v, bias1, bias2, gate, o, lse, dq, dk, dv, dgate, dbias1, dbias2,
+                  accumulate_dbias, workspace, workspace_bytes, stream);
 }
 
 }  // extern "C"

@@ -103,11 +103,13 @@ __global__ void __launch_bounds__(Tiles<DP>::kRows) fwd_kernel(Shape s, const T*
   if (!valid) return;
   const float inv = l > 0.f ? 1.f / l : 0.f;
   T* orow = o + row_off(s, b, i, h);
+  const T* grow = s.gate ? static_cast<const T*>(s.gate) + row_off(s, b, i, h) : nullptr;
   bool nan = false;
 #pragma unroll
   for (int d = 0; d < DP; ++d)
     if (d < s.D) {
-      orow[d] = from_f<T>(acc[d] * inv);
+      // fused output gate (OpenFold): o = sigmoid(G) * O
+      orow[d] = from_f<T>(acc[d] * inv * (grow ? sigmoidf_fast(to_f(grow[d])) : 1.f));
       nan |= isnan(acc[d]);
     }
   const float lv = l > 0.f ? (m + __log2f(l)) * kLn2 : -INFINITY;
@@ -134,6 +136,20 @@ __global__ void delta_kernel(Shape s, const T* __restrict__ dout, const T* __res
     for (int d = 0; d < s.D; ++d) acc = fmaf(to_f(a[d]), to_f(c[d]), acc);
     delta[(b * s.H + h) * s.L + i] = acc;
     flag_if(s.flag, !isfinite(acc));  // NaN in dO (attention_tiled.cpp:209) or O
+  }
+}
+
+// ------------------------------------------- backward of the fused output gate
+// With o = sigmoid(G) * O saved by the forward and dout the gradient of o: the attention backward
+// takes dO = dout * sigmoid(G) (written to dog), dG = dout * o * (1 - sigmoid(G)), and
+// delta = sum_d dO * O = sum_d dout * o (the gate cancels), so no ungated O is ever needed.
+template <typename T>
+__global__ void gate_bwd_kernel(size_t n, const T* __restrict__ dout, const T* __restrict__ o,
+                                const T* __restrict__ gate, T* __restrict__ dog, T* __restrict__ dgate) {
+  for (size_t x = blockIdx.x * (size_t)blockDim.x + threadIdx.x; x < n; x += (size_t)gridDim.x * blockDim.x) {
+    const float sg = sigmoidf_fast(to_f(gate[x])), g = to_f(dout[x]);
+    dog[x] = from_f<T>(g * sg);
+    dgate[x] = from_f<T>(g * to_f(o[x]) * (1.f - sg));
   }
 }
 

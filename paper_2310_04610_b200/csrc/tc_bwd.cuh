@@ -821,7 +821,10 @@ __global__ void __launch_bounds__(kThreads, 1)
 template <int D, typename T, bool SW>
 __global__ void prep_kernel(const T* __restrict__ dout, const T* __restrict__ o, const float* __restrict__ lse,
                             float* __restrict__ lse2, float* __restrict__ delta_p, int B, int L, int H, int Lp,
-                            float4* __restrict__ zero, long long nzero4, int* __restrict__ flag) {
+                            float4* __restrict__ zero, long long nzero4, int* __restrict__ flag,
+                            const T* __restrict__ gate, T* __restrict__ dog, T* __restrict__ dgate) {
+  // gate (fused OpenFold output gate; dout, o are the gated output's gradient and value): also writes
+  // dO = dout * sigmoid(G) for the main kernel and dG = dout * o * (1 - sigmoid(G)); delta = sum dout*o
   constexpr bool swapped = SW;
   ptx::pdl_launch_dependents();
   for (long long x = blockIdx.x * (long long)blockDim.x + threadIdx.x; x < nzero4; x += (long long)gridDim.x * blockDim.x)
@@ -849,6 +852,19 @@ __global__ void prep_kernel(const T* __restrict__ dout, const T* __restrict__ o,
       const T* we = (const T*)&w;
 #pragma unroll
       for (int e = 0; e < 8; ++e) acc = fmaf(to_f(ue[e]), to_f(we[e]), acc);
+      if (gate) {
+        const uint4 gv = __ldg((const uint4*)(gate + r) + c);
+        const T* ge = (const T*)&gv;
+        T go[8], gg[8];
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+          const float sg = sigmoidf_fast(to_f(ge[e])), d = to_f(ue[e]);
+          go[e] = from_f<T>(d * sg);
+          gg[e] = from_f<T>(d * to_f(we[e]) * (1.f - sg));
+        }
+        ((uint4*)(dog + r))[c] = *(const uint4*)go;
+        ((uint4*)(dgate + r))[c] = *(const uint4*)gg;
+      }
     }
     delta_p[orow] = acc;
     flag_if(flag, !isfinite(acc));  // NaN in dO (attention_tiled.cpp:209) or O

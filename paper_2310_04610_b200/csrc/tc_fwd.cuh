@@ -66,6 +66,7 @@ struct FwdParams {
   uint32_t aug_c;    // (c_lo << 16) | c_hi: 16-bit two-term split of 1/scale
   int b1_rows;       // bias1 rows staged in shared memory per Q slot (b1_tma and the budget allows)
   int* flag;         // numeric-check flag (non-finite LSE / NaN O) or null
+  const void* gate;  // output-gate logits (layout of o) or null: o = sigmoid(gate) * attention
   const void* bias1;  // [B, L] or null
   const void* bias2;  // [Bo, H, L, L] (read directly in kBiasGlobal mode)
   void* o;           // [B, L, H, D]
@@ -597,14 +598,31 @@ __global__ void __launch_bounds__(FwdCfg<D>::kThreads, 1)
         if (tid_wg == 0 && wg == 0) trace(p, kTrRowEnd, tl);
         if (i < p.L) {
           const float inv = l_run > 0.f ? __frcp_rn(l_run) : 0.f;
+          const size_t orow = ((p.swapped ? (size_t)i * p.B + b : (size_t)b * p.L + i) * p.H + si.h) * D;
           uint32_t ow[D / 2];
+          if (p.gate) {  // fused output gate (OpenFold): o = sigmoid(G) * O, G read in the row's layout
+            const uint4* g4 = (const uint4*)((const uint16_t*)p.gate + orow);
 #pragma unroll
-          for (int d = 0; d < D; d += 2) {
-            const float o0 = __uint_as_float(ov[d]) * inv, o1 = __uint_as_float(ov[d + 1]) * inv;
-            ow[d / 2] = F16 ? ptx::pack_f16(o0, o1) : ptx::pack_bf16(o0, o1);
+            for (int c = 0; c < D / 8; ++c) {
+              const uint4 gr = __ldg(g4 + c);
+              const uint32_t gw[4] = {gr.x, gr.y, gr.z, gr.w};
+#pragma unroll
+              for (int e = 0; e < 4; ++e) {
+                const int d = c * 8 + 2 * e;
+                const float2 g = unpack2<F16>(gw[e]);
+                const float o0 = __uint_as_float(ov[d]) * inv * sigmoidf_fast(g.x);
+                const float o1 = __uint_as_float(ov[d + 1]) * inv * sigmoidf_fast(g.y);
+                ow[d / 2] = F16 ? ptx::pack_f16(o0, o1) : ptx::pack_bf16(o0, o1);
+              }
+            }
+          } else {
+#pragma unroll
+            for (int d = 0; d < D; d += 2) {
+              const float o0 = __uint_as_float(ov[d]) * inv, o1 = __uint_as_float(ov[d + 1]) * inv;
+              ow[d / 2] = F16 ? ptx::pack_f16(o0, o1) : ptx::pack_bf16(o0, o1);
+            }
           }
-          uint4* dst = (uint4*)((uint16_t*)p.o +
-                                 ((p.swapped ? (size_t)i * p.B + b : (size_t)b * p.L + i) * p.H + si.h) * D);
+          uint4* dst = (uint4*)((uint16_t*)p.o + orow);
 #pragma unroll
           for (int v = 0; v < D / 8; ++v) dst[v] = make_uint4(ow[4 * v], ow[4 * v + 1], ow[4 * v + 2], ow[4 * v + 3]);
           const float lv = l_run > 0.f ? (m_run + __log2f(l_run)) * kLn2 : -INFINITY;

@@ -154,6 +154,7 @@ evo_status launch_fwd(const evo_attn_desc* d, const Shape& s, const void* q, con
   p.bias1 = s.bias1;
   p.bias2 = s.bias2;
   p.o = o;
+  p.gate = s.gate;
   p.lse = lse;
   p.trace = g_trace;
   p.bias_mode = kBiasNone;
@@ -334,8 +335,10 @@ evo_status launch_bwd(const evo_attn_desc* d, const Shape& s, const void* dout, 
   } else {
     tdk = tdv = tb;
   }
+  // with a fused output gate the main kernel reads the gated dO the preamble writes (s.dog)
+  const void* dout_k = s.gate ? s.dog : dout;
   if (!map_bl_hd(&tq, q, s, bk::kBM, dt, 2, err) || !map_bl_hd(&tk, k, s, bk::kBN, dt, 2, err) ||
-      !map_bl_hd(&tv, v, s, bk::kBN, dt, 2, err) || !map_bl_hd(&tdo, dout, s, bk::kBM, dt, 2, err) ||
+      !map_bl_hd(&tv, v, s, bk::kBN, dt, 2, err) || !map_bl_hd(&tdo, dout_k, s, bk::kBM, dt, 2, err) ||
       !(det ? map_f32_rows(&tdq, dqacc, s, nkt * Bw, bk::kBM, err)
             : map_bl_hd(&tdq, dqacc, s, bk::kBM, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, err, true)))
     return EVO_ERR_CUDA;
@@ -390,7 +393,8 @@ evo_status launch_bwd(const evo_attn_desc* d, const Shape& s, const void* dout, 
   } else {
     auto prep = s.swapped ? bk::prep_kernel<D, T, true> : bk::prep_kernel<D, T, false>;
     prep<<<(unsigned)std::min<long long>((prow * Lp + 255) / 256, 148 * 32), 256, 0, st>>>(
-        (const T*)dout, (const T*)o, lse, lse2, delta_p, s.B, s.L, s.H, Lp, zero4, nzero4, s.flag);
+        (const T*)dout, (const T*)o, lse, lse2, delta_p, s.B, s.L, s.H, Lp, zero4, nzero4, s.flag,
+        (const T*)s.gate, (T*)s.dog, (T*)s.dgate);
   }
   ++*launches;
   auto pick = [&](auto safe) {

@@ -143,6 +143,54 @@ def evoformer_attention_backward(dout, q, k, v, o, lse, bias1=None, bias2=None, 
     return dq, dk, dv, db1, db2
 
 
+def evoformer_attention_forward_gated(q, k, v, gate, bias1=None, bias2=None, scale=None, path: str = "auto",
+                                      check_numerics: Optional[bool] = None) -> Tuple[torch.Tensor, torch.Tensor]:
+    """OpenFold-gated attention in one call: o = sigmoid(gate) * attention, the gate
+    applied in the forward kernel's epilogue. gate has the shape and dtype of q. Returns (o, lse)."""
+    lib = N.load()
+    _check_inputs(q, k, v, bias1, bias2)
+    if gate.shape != q.shape or gate.dtype != q.dtype or not gate.is_cuda or not gate.is_contiguous():
+        raise N.ValidationError("gate must be a contiguous CUDA tensor of the shape and dtype of Q")
+    d = make_desc(q, bias1, bias2, scale, path, check_numerics=check_numerics)
+    d.has_gate = 1
+    o = torch.empty_like(q)
+    lse = torch.empty((d.Bo * d.N, d.H, d.L), device=q.device, dtype=torch.float32)
+    wsb = lib.evo_attn_fwd_workspace_size(d)
+    ws = torch.empty(max(wsb, 1), device=q.device, dtype=torch.uint8)
+    N.check(lib.evo_attn_fwd_gated(d, _ptr(q), _ptr(k), _ptr(v), _ptr(bias1), _ptr(bias2), _ptr(gate), _ptr(o),
+                                   _ptr(lse), _ptr(ws), wsb, _stream()))
+    return o, lse
+
+
+def evoformer_attention_backward_gated(dout, q, k, v, gate, o, lse, bias1=None, bias2=None, scale=None,
+                                       need_dbias1: bool = False, need_dbias2: bool = True,
+                                       dbias_dtype: Optional[torch.dtype] = torch.float32, path: str = "auto",
+                                       deterministic: bool = False, check_numerics: Optional[bool] = None):
+    """Backward of evoformer_attention_forward_gated: dout and o are the GATED output's gradient and
+    value. Returns (dq, dk, dv, dgate, dbias1, dbias2); the gate backward is fused into the backward
+    preamble's pass over dout and o."""
+    lib = N.load()
+    _check_inputs(q, k, v, bias1, bias2)
+    for name, t in (("dout", dout), ("o", o), ("gate", gate)):
+        if t.shape != q.shape or t.dtype != q.dtype or not t.is_contiguous():
+            raise N.ValidationError(f"{name} must be contiguous with the shape and dtype of Q")
+    d = make_desc(q, bias1, bias2, scale, path, dbias_dtype, check_numerics, deterministic)
+    d.has_gate = 1
+    if tuple(lse.shape) != (d.Bo * d.N, d.H, d.L) or lse.dtype != torch.float32:
+        raise N.ValidationError(f"lse must be [B, H, L] float32, got {tuple(lse.shape)} {lse.dtype}")
+    dq, dk, dv, dg = (torch.empty_like(q) for _ in range(4))
+    odt = dbias_dtype if dbias_dtype is not None else torch.float32
+    db1 = torch.empty(bias1.shape, device=q.device, dtype=odt) if need_dbias1 and bias1 is not None else None
+    db2 = torch.empty(bias2.shape, device=q.device, dtype=odt) if need_dbias2 and bias2 is not None else None
+    d.need_dbias1 = int(db1 is not None)
+    wsb = lib.evo_attn_bwd_workspace_size(d)
+    ws = torch.empty(max(wsb, 1), device=q.device, dtype=torch.uint8)
+    N.check(lib.evo_attn_bwd_gated(d, _ptr(dout), _ptr(q), _ptr(k), _ptr(v), _ptr(bias1), _ptr(bias2), _ptr(gate),
+                                   _ptr(o), _ptr(lse), _ptr(dq), _ptr(dk), _ptr(dv), _ptr(dg), _ptr(db1), _ptr(db2),
+                                   0, _ptr(ws), wsb, _stream()))
+    return dq, dk, dv, dg, db1, db2
+
+
 def last_launch_count() -> int:
     return int(N.load().evo_attn_last_launch_count())
 
@@ -157,35 +205,47 @@ def resolved_path(q, bias1=None, bias2=None, path="auto", direction: str = "fwd"
 
 
 class EvoformerAttentionFunction(torch.autograd.Function):
-    """Autograd wrapper: forward saves (q, k, v, o, lse) — O(L) extra memory."""
+    """Autograd wrapper: forward saves (q, k, v, o, lse[, gate]) — O(L) extra memory. With a gate the
+    saved o is the gated output (the backward needs nothing else, see evo_attn_bwd_gated)."""
 
     @staticmethod
-    def forward(ctx, q, k, v, bias1, bias2):
+    def forward(ctx, q, k, v, bias1, bias2, gate=None):
         q, k, v = q.contiguous(), k.contiguous(), v.contiguous()
         b1 = bias1.contiguous() if bias1 is not None else None
         b2 = bias2.contiguous() if bias2 is not None else None
-        o, lse = evoformer_attention_forward(q, k, v, b1, b2)
-        ctx.save_for_backward(q, k, v, o, lse, b1, b2)
+        g = gate.contiguous() if gate is not None else None
+        if g is None:
+            o, lse = evoformer_attention_forward(q, k, v, b1, b2)
+        else:
+            o, lse = evoformer_attention_forward_gated(q, k, v, g, b1, b2)
+        ctx.save_for_backward(q, k, v, o, lse, b1, b2, g)
         return o
 
     @staticmethod
     def backward(ctx, grad_o):
-        q, k, v, o, lse, b1, b2 = ctx.saved_tensors
+        q, k, v, o, lse, b1, b2, g = ctx.saved_tensors
         need1 = b1 is not None and ctx.needs_input_grad[3]
         need2 = b2 is not None and ctx.needs_input_grad[4]
-        dq, dk, dv, db1, db2 = evoformer_attention_backward(
-            grad_o.contiguous(), q, k, v, o, lse, b1, b2, need_dbias1=need1, need_dbias2=need2,
+        if g is None:
+            dq, dk, dv, db1, db2 = evoformer_attention_backward(
+                grad_o.contiguous(), q, k, v, o, lse, b1, b2, need_dbias1=need1, need_dbias2=need2,
+                dbias_dtype=q.dtype)
+            return dq, dk, dv, db1, db2, None
+        dq, dk, dv, dg, db1, db2 = evoformer_attention_backward_gated(
+            grad_o.contiguous(), q, k, v, g, o, lse, b1, b2, need_dbias1=need1, need_dbias2=need2,
             dbias_dtype=q.dtype)
-        return dq, dk, dv, db1, db2
+        return dq, dk, dv, db1, db2, dg
 
 
 def DS4Sci_EvoformerAttention(Q: torch.Tensor, K: torch.Tensor, V: torch.Tensor,
-                              biases: Sequence[Optional[torch.Tensor]]) -> torch.Tensor:
+                              biases: Sequence[Optional[torch.Tensor]], gate: Optional[torch.Tensor] = None
+                              ) -> torch.Tensor:
     """DeepSpeed-compatible entry point: Q/K/V [Bo, N, L, H, D]; biases = [mask [Bo, N, 1, 1, L],
-    pair [Bo, 1, H, L, L]] (either may be None or omitted)."""
+    pair [Bo, 1, H, L, L]] (either may be None or omitted). gate (optional, [Bo, N, L, H, D] logits):
+    OpenFold's sigmoid output gate fused into the kernels — returns sigmoid(gate) * attention."""
     biases = list(biases)
     if len(biases) > 2:
         raise N.ValidationError("at most two biases (mask, pair)")
     while len(biases) < 2:
         biases.append(None)
-    return EvoformerAttentionFunction.apply(Q, K, V, biases[0], biases[1])
+    return EvoformerAttentionFunction.apply(Q, K, V, biases[0], biases[1], gate)

@@ -27,12 +27,12 @@ def make_inputs(Bo, Nr, L, H, D, dtype="bf16", bias1=True, bias2=True, seed=0, m
     return tuple(None if a is None else rnd(a) for a in (q, k, v, do, b1, b2))
 
 
-def oracle_fwd_bwd(q, k, v, do, b1, b2, scale=None, need_dbias1=False, tile=(64, 64, 1)):
+def oracle_fwd_bwd(q, k, v, do, b1, b2, scale=None, need_dbias1=False, tile=(64, 64, 1), fmt=None):
     """Oracle (F32 semantics of attention_tiled.cpp) on identically-rounded inputs.
     Returns O [Bo,N,L,H,D], LSE [B,H,L], dQ, dK, dV, dB1 [Bo,N,1,1,L], dB2 [Bo,1,H,L,L]."""
     Bo, Nr, L, H, D = q.shape
     B = Bo * Nr
-    p = O.Problem(B, L, H, D, fmt=O.F32, Bo=Bo, scale=scale, tile_q=tile[0], tile_k=tile[1],
+    p = O.Problem(B, L, H, D, fmt=O.F32 if fmt is None else fmt, Bo=Bo, scale=scale, tile_q=tile[0], tile_k=tile[1],
                   tile_b=tile[2])
     r = lambda a: None if a is None else a.reshape(-1).astype(np.float64)
     o, lse = O.forward(p, r(q), r(k), r(v), r(b1), r(b2))
@@ -62,3 +62,18 @@ def ref_rel_err(got, want) -> float:
 
 
 TOL = {"f32": 1e-4, "bf16": 1e-2, "f16": 1e-2}
+
+
+def sigmoid(x):
+    return 1.0 / (1.0 + np.exp(-np.asarray(x, dtype=np.float64)))
+
+
+def oracle_fwd_bwd_gated(q, k, v, do_g, b1, b2, gate, scale=None, need_dbias1=False, fmt=None):
+    """The fused output gate (OpenFold: o_g = sigmoid(G) * O) composed around the oracle: the oracle
+    computes O and the attention backward with dO = do_g * sigmoid(G); dG = do_g * O * s (1 - s).
+    Returns (o_g, LSE, dQ, dK, dV, dG, dB1, dB2)."""
+    s = sigmoid(gate)
+    do = np.asarray(do_g, np.float64) * s
+    o, lse, dq, dk, dv, db1, db2 = oracle_fwd_bwd(q, k, v, do, b1, b2, scale=scale, need_dbias1=need_dbias1, fmt=fmt)
+    dg = np.asarray(do_g, np.float64) * o * s * (1.0 - s)
+    return o * s, lse, dq, dk, dv, dg, db1, db2
