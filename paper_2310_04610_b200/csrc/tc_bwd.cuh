@@ -114,6 +114,7 @@ struct Params {
   // jt*Bw + wrow) and summed in order after the kernel; dBias1 partials go to db1_part; the dBias2
   // strip flushes of the CTAs sharing a unit are serialised by part through `tickets`.
   int det;
+  int win;          // windowed accumulators (not det): the fp32 dQ (dK, dV) accumulators hold one row window
   int* tickets;     // [units of the window]: strip flushes done (kSoftWG per part), zeroed by the preamble
   float* db1_part;  // [H * nIC][Bw][L] when det and dbias1
   int* flag;        // numeric-check flag (NaN dK / dV) or null
@@ -727,7 +728,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           ptx::named_bar_sync(kEpiBar, 128);
           if (tid_e == 0) {
             if (SAFE && p.det) ptx::tma_store_4d(&tmdQ, stg, 0, u.h, it * kBM, u.jt * Bw + wrow);  // key tile jt's slot
-            else ptx::tma_reduce_add_4d(&tmdQ, stg, 0, u.h, it * kBM, b);
+            else ptx::tma_reduce_add_4d(&tmdQ, stg, 0, u.h, it * kBM, (SAFE && p.win) ? wrow : b);
             ptx::bulk_commit();
             trace(p, kTbDqOut, step);
           }
@@ -775,8 +776,9 @@ __global__ void __launch_bounds__(kThreads, 1)
               ptx::tma_store_4d(&tmdK, stg, 0, u.h, u.jt * kBN, u.ic * Bw + wrow);
               ptx::tma_store_4d(&tmdV, stg + 64 * D, 0, u.h, u.jt * kBN, u.ic * Bw + wrow);
             } else {
-              ptx::tma_reduce_add_4d(&tmdK, stg, 0, u.h, u.jt * kBN, b);
-              ptx::tma_reduce_add_4d(&tmdV, stg + 64 * D, 0, u.h, u.jt * kBN, b);
+              const int ar = (SAFE && p.win) ? wrow : b;
+              ptx::tma_reduce_add_4d(&tmdK, stg, 0, u.h, u.jt * kBN, ar);
+              ptx::tma_reduce_add_4d(&tmdV, stg + 64 * D, 0, u.h, u.jt * kBN, ar);
             }
             ptx::bulk_commit();
             ptx::bulk_wait_read<0>();  // the buffer is the next dQ step's
@@ -932,7 +934,8 @@ __global__ void dq_convert_kernel(const float* __restrict__ acc, T* __restrict__
 template <typename T, bool SW>
 __global__ void det_convert_kernel(const float* __restrict__ part, int np, size_t pstride, T* __restrict__ out,
                                    size_t n, float scale, int B, int L, int HD, int N, int n0w, int nw,
-                                   int* __restrict__ flag) {
+                                   int* __restrict__ flag, int zero_after) {
+  // zero_after (windowed accumulators, np == 1): the accumulator is left zeroed for the next window
   ptx::pdl_wait();  // programmatic dependent of the main kernel
   ptx::pdl_launch_dependents();
   constexpr bool F16 = std::is_same<T, __half>::value;
@@ -947,6 +950,10 @@ __global__ void det_convert_kernel(const float* __restrict__ part, int np, size_
       const float4 u = *(const float4*)(part + (size_t)k * pstride + x), w = *(const float4*)(part + (size_t)k * pstride + x + 4);
       a[0] += u.x; a[1] += u.y; a[2] += u.z; a[3] += u.w; a[4] += w.x; a[5] += w.y; a[6] += w.z; a[7] += w.w;
     }
+    if (zero_after) {
+      *(float4*)(part + x) = make_float4(0.f, 0.f, 0.f, 0.f);
+      *(float4*)(part + x + 4) = make_float4(0.f, 0.f, 0.f, 0.f);
+    }
     bool nan = false;
     uint32_t wv[4];
 #pragma unroll
@@ -956,10 +963,16 @@ __global__ void det_convert_kernel(const float* __restrict__ part, int np, size_
                   : ptx::pack_bf16(a[2 * e] * scale, a[2 * e + 1] * scale);
     }
     flag_if(flag, nan);
-    const size_t wrow = x / rowlen, rem = x - wrow * rowlen;
-    const size_t ob = wrow / nw, b = ob * N + n0w + (wrow - ob * nw);
-    const size_t i = rem / HD, e = rem - i * HD;
-    const size_t off = SW ? (i * B + b) * HD + e : (b * L + i) * HD + e;
+    size_t off;
+    if constexpr (!SW) {  // canonical: the window of outer batch ob is one contiguous block of rows
+      const size_t blk = (size_t)nw * rowlen;
+      const size_t ob = blk >= n ? 0 : (size_t)((uint32_t)x / (uint32_t)blk);  // window < 2^32 elements
+      off = x + (ob * (size_t)(N - nw) + n0w) * rowlen;
+    } else {  // raw [L, B, H, D] (Bo == 1): row b = n0w + x / rowlen, scattered by i
+      const uint32_t wrow = (uint32_t)x / (uint32_t)rowlen, rem = (uint32_t)x - wrow * (uint32_t)rowlen;
+      const uint32_t i = rem / (uint32_t)HD, e = rem - i * (uint32_t)HD;
+      off = ((size_t)i * B + n0w + wrow) * HD + e;
+    }
     if (((uintptr_t)(out + off) & 15) == 0) {
       *(uint4*)(out + off) = make_uint4(wv[0], wv[1], wv[2], wv[3]);
     } else {

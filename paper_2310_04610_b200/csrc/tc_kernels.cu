@@ -237,6 +237,9 @@ size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
 //                 [nIC][Bw, L, H, D], dBias1 [H * nIC][Bw][L] — plus the dBias2 flush tickets of
 //                 every window; windows of nw rows per outer batch keep the partials under kDetCap.
 constexpr size_t kDetCap = (size_t)2 << 30;
+// default mode: the fp32 accumulators (dQ; dK, dV when chunked) cover all rows when they fit kAccCap,
+// else one row window at a time (C5: 3 x 1 MB per row -> windows of ~340 rows, 1 GB instead of 6.4 GB)
+constexpr size_t kAccCap = (size_t)1 << 30;
 struct BwdScratch {
   size_t dq, dk, dv, lse2, delta, db1p, tickets, total;
   int nw, nwin;  // deterministic row window (rows per outer batch), number of windows
@@ -264,7 +267,14 @@ BwdScratch bwd_scratch_layout(const evo_attn_desc* d) {
     db1p = db1 ? align256((size_t)d->H * nic * Bw * d->L * 4) : 0;
     tickets = align256((size_t)w.nwin * d->Bo * d->H * nkt * nic * 4);
   } else {
-    dq_bytes = align256(B * row);
+    const size_t per = row * (chunked ? 3 : 1);
+    size_t cap = kAccCap;
+    if (const char* e = getenv("EVO_BWD_ACC_CAP_MB")) cap = (size_t)atoll(e) << 20;  // experiments
+    w.nw = (int)std::max<int64_t>(1, std::min<int64_t>(d->N, (int64_t)(cap / (per * d->Bo))));
+    if (const char* e = getenv("EVO_BWD_WINDOW_ROWS"))  // test hook: force the row window (0: all rows)
+      w.nw = atoi(e) > 0 ? std::min(w.nw, atoi(e)) : (int)d->N;
+    w.nwin = (int)((d->N + w.nw - 1) / w.nw);
+    dq_bytes = align256((size_t)d->Bo * w.nw * row);
     kv_bytes = chunked ? dq_bytes : 0;  // dK/dV accumulators when the query axis is chunked
   }
   w.dq = 0;
@@ -315,6 +325,7 @@ evo_status launch_bwd(const evo_attn_desc* d, const Shape& s, const void* dout, 
   const CUtensorMapDataType dt = F16 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT16 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16;
   const BwdScratch w = bwd_scratch_layout(d);
   const bool det = d->deterministic != 0;
+  const bool win = !det && w.nwin > 1;  // windowed accumulators
   char* ws = (char*)scratch;
   float* dqacc = (float*)(ws + w.dq);
   float* lse2 = (float*)(ws + w.lse2);
@@ -328,7 +339,8 @@ evo_status launch_bwd(const evo_attn_desc* d, const Shape& s, const void* dout, 
   const int nkt = bwd_nkt(d), nic = bwd_nic(d, want_db1);
   const long long Bw = (long long)d->Bo * w.nw;  // rows of a (full) deterministic window
   if (dkv_reduce) {
-    const bool ok = det ? map_f32_rows(&tdk, dkacc, s, nic * Bw, bk::kBN, err) && map_f32_rows(&tdv, dvacc, s, nic * Bw, bk::kBN, err)
+    const long long kvrows = det ? nic * Bw : Bw;
+    const bool ok = (det || win) ? map_f32_rows(&tdk, dkacc, s, kvrows, bk::kBN, err) && map_f32_rows(&tdv, dvacc, s, kvrows, bk::kBN, err)
                         : map_bl_hd(&tdk, dkacc, s, bk::kBN, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, err, true) &&
                               map_bl_hd(&tdv, dvacc, s, bk::kBN, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, err, true);
     if (!ok) return EVO_ERR_CUDA;
@@ -339,7 +351,7 @@ evo_status launch_bwd(const evo_attn_desc* d, const Shape& s, const void* dout, 
   const void* dout_k = s.gate ? s.dog : dout;
   if (!map_bl_hd(&tq, q, s, bk::kBM, dt, 2, err) || !map_bl_hd(&tk, k, s, bk::kBN, dt, 2, err) ||
       !map_bl_hd(&tv, v, s, bk::kBN, dt, 2, err) || !map_bl_hd(&tdo, dout_k, s, bk::kBM, dt, 2, err) ||
-      !(det ? map_f32_rows(&tdq, dqacc, s, nkt * Bw, bk::kBM, err)
+      !((det || win) ? map_f32_rows(&tdq, dqacc, s, det ? nkt * Bw : Bw, bk::kBM, err)
             : map_bl_hd(&tdq, dqacc, s, bk::kBM, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, err, true)))
     return EVO_ERR_CUDA;
   if (s.bias2 && !map_bias(&tb, s.bias2, s, (int)d->Bo, dt, err)) return EVO_ERR_CUDA;
@@ -367,6 +379,7 @@ evo_status launch_bwd(const evo_attn_desc* d, const Shape& s, const void* dout, 
   p.has_bias2 = s.bias2 != nullptr;
   p.trace = g_trace_bwd;
   p.det = det ? 1 : 0;
+  p.win = win ? 1 : 0;
   p.db1_part = (float*)(ws + w.db1p);
   p.flag = s.flag;
   // bias1 (and the key mask past L) enter S through one extra K=16 MMA step: A_aug rows hold a
@@ -402,14 +415,14 @@ evo_status launch_bwd(const evo_attn_desc* d, const Shape& s, const void* dout, 
     return s.swapped ? (dkv_reduce ? bk::bwd_kernel<D, F16, true, true, S> : bk::bwd_kernel<D, F16, false, true, S>)
                      : (dkv_reduce ? bk::bwd_kernel<D, F16, true, false, S> : bk::bwd_kernel<D, F16, false, false, S>);
   };
-  auto kern = (det || s.flag) ? pick(std::true_type{}) : pick(std::false_type{});
+  auto kern = (det || win || s.flag) ? pick(std::true_type{}) : pick(std::false_type{});
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   const int G = sm_count();
   auto pdl_launch = [&](auto fn, dim3 grid, dim3 block, size_t shm, auto... args) {
     cudaLaunchConfig_t cfg = {};  // programmatic dependent launch: the prologue overlaps the predecessor's tail
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    attr[0].val.programmaticStreamSerializationAllowed = getenv("EVO_NO_PDL") ? 0 : 1;
     cfg.gridDim = grid;
     cfg.blockDim = block;
     cfg.dynamicSmemBytes = shm;
@@ -421,11 +434,11 @@ evo_status launch_bwd(const evo_attn_desc* d, const Shape& s, const void* dout, 
   };
   const long long units = (long long)p.Bo * p.H * p.nKT * p.nIC;
   const int HD = s.H * D;
-  for (int win = 0; win < w.nwin; ++win) {
-    p.n0w = win * w.nw;
+  for (int wi = 0; wi < w.nwin; ++wi) {
+    p.n0w = wi * w.nw;
     p.nw = std::min<int>(w.nw, s.N - p.n0w);
     p.total = units * p.nw;
-    p.tickets = det ? (int*)(ws + w.tickets) + (size_t)win * units : nullptr;
+    p.tickets = det ? (int*)(ws + w.tickets) + (size_t)wi * units : nullptr;
     long long grid = std::min<long long>(p.total, G);
     p.aligned = 0;
     p.split = 1;
@@ -439,15 +452,35 @@ evo_status launch_bwd(const evo_attn_desc* d, const Shape& s, const void* dout, 
       // ordered sums of this window's partial slots (dQ over key tiles; dK / dV over query chunks)
       const size_t n = (size_t)p.Bo * p.nw * s.L * HD, pstride = n;
       const unsigned cg = (unsigned)std::min<size_t>((n / 8 + 255) / 256, 148 * 16);
-      auto conv = [&](const float* part, int np, void* out, float scale) {
+      auto conv = [&](float* part, int np, void* out, float scale) {
         pdl_launch(s.swapped ? bk::det_convert_kernel<T, true> : bk::det_convert_kernel<T, false>, dim3(cg), dim3(256),
-                   0, part, np, pstride, (T*)out, n, scale, s.B, s.L, HD, s.N, p.n0w, p.nw, s.flag);
+                   0, (const float*)part, np, pstride, (T*)out, n, scale, s.B, s.L, HD, s.N, p.n0w, p.nw, s.flag, 0);
       };
       conv(dqacc, nkt, dq, s.scale);
       if (dkv_reduce) {
         conv(dkacc, nic, dk, s.scale);
         conv(dvacc, nic, dv, 1.f);
       }
+    } else if (win) {
+      // this window's accumulators into their rows (the streaming conversion, per outer batch: the rows
+      // of one window and outer batch are contiguous), then zeroed for the next window
+      const size_t rowlen = (size_t)s.L * HD, nob = (size_t)p.nw * rowlen;
+      const unsigned cg = (unsigned)std::min<size_t>((nob / 8 + 255) / 256, 148 * 16);
+      auto conv = [&](const float* acc, void* out, float scale) {
+        for (int ob = 0; ob < p.Bo; ++ob) {
+          const size_t shift = s.swapped ? (size_t)p.n0w * HD : ((size_t)ob * s.N + p.n0w) * rowlen;
+          pdl_launch(s.swapped ? bk::dq_convert_kernel<T, true> : bk::dq_convert_kernel<T, false>, dim3(cg), dim3(256),
+                     0, acc + ob * nob, (T*)out + shift, nob, scale, s.B, s.L, HD, s.flag);
+        }
+      };
+      conv(dqacc, dq, s.scale);
+      if (dkv_reduce) {
+        conv(dkacc, dk, s.scale);
+        conv(dvacc, dv, 1.f);
+      }
+      if (wi + 1 < w.nwin) cudaMemsetAsync(dqacc, 0, dkv_reduce ? w.lse2 : w.dk, st);
+    }
+    if (det) {
       if (dbias1) {  // dBias1 partials of (head, chunk) slots in order, per outer batch of the window
         const size_t nl = (size_t)p.nw * s.L;
         for (int ob = 0; ob < p.Bo; ++ob) {
@@ -458,7 +491,7 @@ evo_status launch_bwd(const evo_attn_desc* d, const Shape& s, const void* dout, 
       }
     }
   }
-  if (!det) {
+  if (!det && !win) {
     const size_t n = (size_t)s.B * s.L * HD;
     const unsigned cg = (unsigned)std::min<size_t>((n / 8 + 255) / 256, 148 * 16);
     auto convert = [&](const float* acc, void* out, float scale) {  // programmatic dependents of the main kernel

@@ -256,3 +256,29 @@ def test_long_l_forward_without_bias1_staging():
     wo, wl = O.forward(p, r(q), r(k), r(v), r(b1), r(b2))
     assert nmax_err(o.float().cpu().numpy(), wo.reshape(q.shape)) <= 1e-2
     assert nmax_err(lse.cpu().numpy(), wl.transpose(1, 0, 2)) <= 1e-2
+
+
+# ------------------------------------------------------------------------------ bounded workspace
+@pytest.mark.parametrize("shape", [(1, 7, 640, 2, 32), (2, 5, 256, 2, 32)])
+def test_windowed_accumulators(monkeypatch, shape):
+    # the default (unordered) backward bounds its fp32 accumulators to one row window at a time when the
+    # whole problem's would exceed the cap (C5); forced here to windows of 2 rows (ragged last window,
+    # chunked and unchunked query axis, outer batch) — same results as the oracle
+    import paper_2310_04610_b200 as E
+
+    inp = make_inputs(*shape, dtype="bf16", seed=31)
+    monkeypatch.setenv("EVO_BWD_WINDOW_ROWS", "2")
+    got = _bwd(inp, "bf16", False)
+    want = oracle_fwd_bwd(*inp)
+    for name, g, w in zip(["dQ", "dK", "dV", "dBias2"], got, [want[2], want[3], want[4], want[6]]):
+        assert nmax_err(g.float().cpu().numpy(), w) <= TOL["bf16"], name
+    monkeypatch.delenv("EVO_BWD_WINDOW_ROWS")
+    q = _t(inp[0])
+    from paper_2310_04610_b200 import _native as N
+    from paper_2310_04610_b200.evoformer_attention import make_desc
+
+    lib = N.load()
+    d = make_desc(q, _t(inp[4]), _t(inp[5]), None)
+    full = lib.evo_attn_bwd_workspace_size(d)
+    monkeypatch.setenv("EVO_BWD_WINDOW_ROWS", "2")
+    assert lib.evo_attn_bwd_workspace_size(d) < full
