@@ -47,8 +47,8 @@ typedef enum {
 typedef enum { EVO_F32 = 0, EVO_BF16 = 1, EVO_F16 = 2 } evo_dtype;
 
 /* Kernel family selection. AUTO picks tcgen05 (sm_100a tensor cores) for
- * bf16/f16 with D in {16, 32, 64} (forward) and D in {16, 32}, L % 8 == 0
- * (backward), and the SIMT (FFMA) kernels otherwise
+ * bf16/f16 with D in {8, 16, 32, 64} (forward) and D in {8, 16, 32}, L % 8 == 0
+ * (backward; D = 8 runs the D = 16 kernels on zero-padded TMA boxes), and the SIMT (FFMA) kernels otherwise
  * (fp32 must not use TF32: it fails the 1e-4 parity bar). */
 typedef enum { EVO_PATH_AUTO = 0, EVO_PATH_SIMT = 1, EVO_PATH_TCGEN05 = 2 } evo_path;
 

@@ -14,10 +14,13 @@
 //     dbias (H, L, L) in F32 (AccumMode::UpcastF32);
 //   * ledger records under the reference labels: "tiled/stats" (kept until the caller frees it),
 //     "tiled/delta" and "tiled/work/..." (transient) — with the device working set as the bytes.
+//   * AccumPolicy::deterministic (attention_tiled.hpp:35-44, the reference default) -> the C-ABI's
+//     deterministic backward (every cross-CTA reduction in a fixed order: two runs are bit-identical,
+//     SPEC.md:211); non-finite logits (attention_tiled.cpp:125-127) -> the kernels' numeric checks.
 // Differences (documented in INTEGRATION.md): F64 problems and AccumMode::NativeFormat are not
 // served by the GPU kernels (ValidationError); TileConfig is validated but does not steer the kernels, which use
-// their own B200 tiling, results are tile-independent within the format tolerance;
-// the dBias reduction order across CTAs is fixed per launch shape but is an fp32 sum of partials.
+// their own B200 tiling, results are tile-independent within the format tolerance; the
+// deterministic order is the kernels' own fixed order, not the reference's ascending-b recurrence.
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -164,6 +167,7 @@ evo_attn_desc describe(const AttentionProblem& p) {
   d.has_bias2 = p.bias.has_value() ? 1 : 0;
   d.dbias_dtype = EVO_F32;
   d.path = EVO_PATH_AUTO;
+  d.check_numerics = 1;  // NumericError for non-finite logit rows, as attention_tiled.cpp:125-127
   return d;
 }
 
@@ -250,7 +254,8 @@ AttentionGrads attn_backward_tiled(const AttentionProblem& p, const Tensor& outp
   if (policy.mode != AccumMode::UpcastF32)
     throw ValidationError("the GPU backend reduces the bias gradient in F32 (AccumMode::UpcastF32)");
 
-  const evo_attn_desc d = describe(p);
+  evo_attn_desc d = describe(p);
+  d.deterministic = policy.deterministic ? 1 : 0;  // AccumPolicy::deterministic (attention_tiled.cpp:246-252)
   DeviceBuffer q(p.query, d.dtype), k(p.key, d.dtype), v(p.value, d.dtype);
   DeviceBuffer o(output, d.dtype), dout(grad_output, d.dtype);
   std::optional<DeviceBuffer> b2;

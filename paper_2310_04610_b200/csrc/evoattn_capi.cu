@@ -53,7 +53,7 @@ bool scale_fits_16bit(const evo_attn_desc* d) {
 }
 
 bool tc_eligible(const evo_attn_desc* d) {
-  return d->dtype != EVO_F32 && (d->D == 16 || d->D == 32 || d->D == 64) && scale_fits_16bit(d) &&
+  return d->dtype != EVO_F32 && (d->D == 8 || d->D == 16 || d->D == 32 || d->D == 64) && scale_fits_16bit(d) &&
          evo::tc::device_supported();
 }
 
@@ -105,7 +105,7 @@ size_t elem_bytes(const evo_attn_desc* d) { return d->dtype == EVO_F32 ? 4 : 2; 
 // without one (sizing only) the tcgen05 envelope is assumed.
 bool simt_bwd_path(const evo_attn_desc* d) {
   if (d->path == EVO_PATH_SIMT) return true;
-  const bool tc = d->dtype != EVO_F32 && (d->D == 16 || d->D == 32) && d->L % 8 == 0 && scale_fits_16bit(d);
+  const bool tc = d->dtype != EVO_F32 && (d->D == 8 || d->D == 16 || d->D == 32) && d->L % 8 == 0 && scale_fits_16bit(d);
   return !tc;
 }
 

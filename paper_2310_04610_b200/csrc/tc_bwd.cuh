@@ -64,7 +64,8 @@ constexpr uint32_t kDb1Col = 384;
 #define EVO_BWD_POLY 0
 #endif
 #ifndef EVO_BWD_EXP
-#define EVO_BWD_EXP 0  // timing experiments only (wrong results), bit mask: 1 no dK/dV MMAs, 2 no dQ MMA, 4 no bias LDS, 8 no P/dS stores
+#define EVO_BWD_EXP 0  // timing experiments only (wrong results), bit mask: 1 no dK/dV MMAs, 2 no dQ MMA, 4 no bias LDS,
+                       // 8 no P/dS stores, 16 no exponentials, 32 no dQ staging/reduce, 64 no dBias2 strip MMAs
 #endif  // dBias1 column sums (M=64, 16 columns) when requested: chunks of <= 2 q-tiles
 
 template <int D, bool CH>
@@ -118,6 +119,7 @@ struct Params {
   int* tickets;     // [units of the window]: strip flushes done (kSoftWG per part), zeroed by the preamble
   float* db1_part;  // [H * nIC][Bw][L] when det and dbias1
   int* flag;        // numeric-check flag (NaN dK / dV) or null
+  int dreal;        // head dim in memory (D = 16 kernels serve D = 8 with zero-padded TMA boxes)
 };
 
 // CTA-0 timeline of steps [kTrFirst, kTrFirst + 64): 8 events x 64 steps (bring-up aid)
@@ -440,7 +442,7 @@ __global__ void __launch_bounds__(kThreads, 1)
               // dS block kk (K-major, 16 keys) times a 16 x 16 identity; the unit's first row initialises
               const uint32_t st = tmem + kStripCol + (uint32_t)(it - (CH ? u.it0 : 0)) * 64;
 #pragma unroll
-              for (int kk = 0; kk < kBN / 16; ++kk) {
+              for (int kk = 0; kk < ((EVO_BWD_EXP & 64) ? 0 : kBN / 16); ++kk) {
                 if (EVO_BWD_DS_TMEM)
                   ptx::mma_ts(st + kk * 16, tmem + sb * 128 + kk * 16, bIdent, idStrip, a > 0 ? 1u : 0u);
                 else
@@ -603,7 +605,9 @@ __global__ void __launch_bounds__(kThreads, 1)
                 const float2 bb = __ffma2_rn(unpack2<F16>(wv[e]), lg2, nl);  // bias2 * log2e - lse * log2e
                 const float2 x = __ffma2_rn(make_float2(__uint_as_float(sv[k]), __uint_as_float(sv[k + 1])), scl2, bb);
                 float2 pr;
-                if (EVO_BWD_POLY && e == 3) {
+                if (EVO_BWD_EXP & 16) {
+                  pr = x;
+                } else if (EVO_BWD_POLY && e == 3) {
                   pr = ex2_poly2(x);  // one pair in four on the FMA pipe (relieves MUFU)
                 } else {
                   pr.x = ex2(x.x);
@@ -713,6 +717,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           ptx::tc_fence_before();
           ptx::mbar_arrive(dq_free);
           float* stg = sDq + (C::kDqBufs == 2 ? (step & 1) * kBM * D : 0);
+          if (EVO_BWD_EXP & 32) { ++step; continue; }
           if (tid_e == 0) {  // the reduce that last used this staging tile has read it
             if constexpr (C::kDqBufs == 2) ptx::bulk_wait_read<1>(); else ptx::bulk_wait_read<0>();
           }
@@ -800,9 +805,10 @@ __global__ void __launch_bounds__(kThreads, 1)
             ow[d / 2] = F16 ? ptx::pack_f16(__uint_as_float(v[d]) * sc, __uint_as_float(v[d + 1]) * sc)
                             : ptx::pack_bf16(__uint_as_float(v[d]) * sc, __uint_as_float(v[d + 1]) * sc);
           uint4* dst = (uint4*)((uint16_t*)(isk ? p.dk : p.dv) +
-                                   ((SW ? (size_t)j * p.B + b : (size_t)b * p.L + j) * p.H + u.h) * D);
+                                   ((SW ? (size_t)j * p.B + b : (size_t)b * p.L + j) * p.H + u.h) * p.dreal);
 #pragma unroll
-          for (int q = 0; q < D / 8; ++q) dst[q] = make_uint4(ow[4 * q], ow[4 * q + 1], ow[4 * q + 2], ow[4 * q + 3]);
+          for (int q = 0; q < D / 8; ++q)
+            if (q * 8 < p.dreal) dst[q] = make_uint4(ow[4 * q], ow[4 * q + 1], ow[4 * q + 2], ow[4 * q + 3]);
         }
       }
     }

@@ -64,18 +64,21 @@ CUtensorMapSwizzle swz(int row_bytes) {
 }
 
 // (B, L, H, D) row-major as a 4-D map (D, H, L, B); box (D, 1, rows, 1).
+// box_d: the kernel's head dim (D = 8 problems run the D = 16 kernels: the 16-wide box reads 8 real
+// columns and TMA zero-fills the rest; stores / reduces of the padded columns are clipped)
 bool map_bl_hd(CUtensorMap* m, const void* base, const Shape& s, int rows, CUtensorMapDataType dt,
-               int esize, std::string* err, bool canonical = false) {
+               int esize, std::string* err, bool canonical = false, int box_d = 0) {
+  if (box_d == 0) box_d = s.D;
   const bool swapped = s.swapped && !canonical;
   cuuint64_t dims[4] = {(cuuint64_t)s.D, (cuuint64_t)s.H, (cuuint64_t)s.L, (cuuint64_t)s.B};
   // swapped (raw msa_col / tri_end layout, (L, B, H, D)): the L and B strides trade places
   const cuuint64_t hd = (cuuint64_t)s.H * s.D * esize;
   cuuint64_t strides[3] = {(cuuint64_t)s.D * esize, swapped ? hd * (cuuint64_t)s.B : hd,
                            swapped ? hd : hd * (cuuint64_t)s.L};
-  cuuint32_t box[4] = {(cuuint32_t)s.D, 1, (cuuint32_t)rows, 1};
+  cuuint32_t box[4] = {(cuuint32_t)box_d, 1, (cuuint32_t)rows, 1};
   cuuint32_t es[4] = {1, 1, 1, 1};
   CUresult r = encode_fn()(m, dt, 4, const_cast<void*>(base), dims, strides, box, es,
-                           CU_TENSOR_MAP_INTERLEAVE_NONE, swz(s.D * esize), CU_TENSOR_MAP_L2_PROMOTION_NONE,
+                           CU_TENSOR_MAP_INTERLEAVE_NONE, swz(box_d * esize), CU_TENSOR_MAP_L2_PROMOTION_NONE,
                            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) {
     *err = "cuTensorMapEncodeTiled (B,L,H,D) failed: " + std::to_string((int)r);
@@ -141,8 +144,8 @@ evo_status launch_fwd(const evo_attn_desc* d, const Shape& s, const void* q, con
   const CUtensorMapDataType dt = F16 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT16 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16;
   CUtensorMap tq, tk, tv, tb;
   memset(&tb, 0, sizeof(tb));
-  if (!map_bl_hd(&tq, q, s, kBM, dt, 2, err) || !map_bl_hd(&tk, k, s, kBN, dt, 2, err) ||
-      !map_bl_hd(&tv, v, s, kBN, dt, 2, err))
+  if (!map_bl_hd(&tq, q, s, kBM, dt, 2, err, false, D) || !map_bl_hd(&tk, k, s, kBN, dt, 2, err, false, D) ||
+      !map_bl_hd(&tv, v, s, kBN, dt, 2, err, false, D))
     return EVO_ERR_CUDA;
   FwdParams p{};
   p.B = s.B; p.N = s.N; p.L = s.L; p.H = s.H; p.Bo = (int)d->Bo;
@@ -155,6 +158,7 @@ evo_status launch_fwd(const evo_attn_desc* d, const Shape& s, const void* q, con
   p.bias2 = s.bias2;
   p.o = o;
   p.gate = s.gate;
+  p.dreal = s.D;
   p.lse = lse;
   p.trace = g_trace;
   p.bias_mode = kBiasNone;
@@ -289,14 +293,15 @@ BwdScratch bwd_scratch_layout(const evo_attn_desc* d) {
 }
 
 // fp32 [rows, L, H, D] (canonical) as a 4-D map (D, H, L, rows), box (D, 1, box_rows, 1), row-size swizzle
-bool map_f32_rows(CUtensorMap* m, void* base, const Shape& s, long long rows, int box_rows, std::string* err) {
+bool map_f32_rows(CUtensorMap* m, void* base, const Shape& s, long long rows, int box_rows, std::string* err,
+                  int box_d) {
   cuuint64_t dims[4] = {(cuuint64_t)s.D, (cuuint64_t)s.H, (cuuint64_t)s.L, (cuuint64_t)rows};
   const cuuint64_t hd = (cuuint64_t)s.H * s.D * 4;
   cuuint64_t strides[3] = {(cuuint64_t)s.D * 4, hd, hd * (cuuint64_t)s.L};
-  cuuint32_t box[4] = {(cuuint32_t)s.D, 1, (cuuint32_t)box_rows, 1};
+  cuuint32_t box[4] = {(cuuint32_t)box_d, 1, (cuuint32_t)box_rows, 1};
   cuuint32_t es[4] = {1, 1, 1, 1};
   CUresult r = encode_fn()(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, base, dims, strides, box, es,
-                           CU_TENSOR_MAP_INTERLEAVE_NONE, swz(s.D * 4), CU_TENSOR_MAP_L2_PROMOTION_NONE,
+                           CU_TENSOR_MAP_INTERLEAVE_NONE, swz(box_d * 4), CU_TENSOR_MAP_L2_PROMOTION_NONE,
                            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) {
     *err = "cuTensorMapEncodeTiled (fp32 partials) failed: " + std::to_string((int)r);
@@ -340,19 +345,20 @@ evo_status launch_bwd(const evo_attn_desc* d, const Shape& s, const void* dout, 
   const long long Bw = (long long)d->Bo * w.nw;  // rows of a (full) deterministic window
   if (dkv_reduce) {
     const long long kvrows = det ? nic * Bw : Bw;
-    const bool ok = (det || win) ? map_f32_rows(&tdk, dkacc, s, kvrows, bk::kBN, err) && map_f32_rows(&tdv, dvacc, s, kvrows, bk::kBN, err)
-                        : map_bl_hd(&tdk, dkacc, s, bk::kBN, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, err, true) &&
-                              map_bl_hd(&tdv, dvacc, s, bk::kBN, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, err, true);
+    const bool ok = (det || win) ? map_f32_rows(&tdk, dkacc, s, kvrows, bk::kBN, err, D) &&
+                                       map_f32_rows(&tdv, dvacc, s, kvrows, bk::kBN, err, D)
+                                 : map_bl_hd(&tdk, dkacc, s, bk::kBN, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, err, true, D) &&
+                                       map_bl_hd(&tdv, dvacc, s, bk::kBN, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, err, true, D);
     if (!ok) return EVO_ERR_CUDA;
   } else {
     tdk = tdv = tb;
   }
   // with a fused output gate the main kernel reads the gated dO the preamble writes (s.dog)
   const void* dout_k = s.gate ? s.dog : dout;
-  if (!map_bl_hd(&tq, q, s, bk::kBM, dt, 2, err) || !map_bl_hd(&tk, k, s, bk::kBN, dt, 2, err) ||
-      !map_bl_hd(&tv, v, s, bk::kBN, dt, 2, err) || !map_bl_hd(&tdo, dout_k, s, bk::kBM, dt, 2, err) ||
-      !((det || win) ? map_f32_rows(&tdq, dqacc, s, det ? nkt * Bw : Bw, bk::kBM, err)
-            : map_bl_hd(&tdq, dqacc, s, bk::kBM, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, err, true)))
+  if (!map_bl_hd(&tq, q, s, bk::kBM, dt, 2, err, false, D) || !map_bl_hd(&tk, k, s, bk::kBN, dt, 2, err, false, D) ||
+      !map_bl_hd(&tv, v, s, bk::kBN, dt, 2, err, false, D) || !map_bl_hd(&tdo, dout_k, s, bk::kBM, dt, 2, err, false, D) ||
+      !((det || win) ? map_f32_rows(&tdq, dqacc, s, det ? nkt * Bw : Bw, bk::kBM, err, D)
+            : map_bl_hd(&tdq, dqacc, s, bk::kBM, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, err, true, D)))
     return EVO_ERR_CUDA;
   if (s.bias2 && !map_bias(&tb, s.bias2, s, (int)d->Bo, dt, err)) return EVO_ERR_CUDA;
   bk::Params p{};
@@ -380,6 +386,7 @@ evo_status launch_bwd(const evo_attn_desc* d, const Shape& s, const void* dout, 
   p.trace = g_trace_bwd;
   p.det = det ? 1 : 0;
   p.win = win ? 1 : 0;
+  p.dreal = s.D;
   p.db1_part = (float*)(ws + w.db1p);
   p.flag = s.flag;
   // bias1 (and the key mask past L) enter S through one extra K=16 MMA step: A_aug rows hold a
@@ -404,7 +411,8 @@ evo_status launch_bwd(const evo_attn_desc* d, const Shape& s, const void* dout, 
     bk::pad_rows_kernel<<<(unsigned)std::min<long long>((prow * Lp + 255) / 256, 148 * 16), 256, 0, st>>>(
         lse, delta, lse2, delta_p, s.L, Lp, prow, zero4, nzero4);
   } else {
-    auto prep = s.swapped ? bk::prep_kernel<D, T, true> : bk::prep_kernel<D, T, false>;
+    auto prep = s.D == 8 ? (s.swapped ? bk::prep_kernel<8, T, true> : bk::prep_kernel<8, T, false>)
+                         : (s.swapped ? bk::prep_kernel<D, T, true> : bk::prep_kernel<D, T, false>);
     prep<<<(unsigned)std::min<long long>((prow * Lp + 255) / 256, 148 * 32), 256, 0, st>>>(
         (const T*)dout, (const T*)o, lse, lse2, delta_p, s.B, s.L, s.H, Lp, zero4, nzero4, s.flag,
         (const T*)s.gate, (T*)s.dog, (T*)s.dgate);
@@ -433,7 +441,7 @@ evo_status launch_bwd(const evo_attn_desc* d, const Shape& s, const void* dout, 
     ++*launches;
   };
   const long long units = (long long)p.Bo * p.H * p.nKT * p.nIC;
-  const int HD = s.H * D;
+  const int HD = s.H * s.D;
   for (int wi = 0; wi < w.nwin; ++wi) {
     p.n0w = wi * w.nw;
     p.nw = std::min<int>(w.nw, s.N - p.n0w);
@@ -547,11 +555,12 @@ size_t bwd_scratch_bytes(const evo_attn_desc* d) { return bwd_scratch_layout(d).
 // L > 384 splits the query axis into chunks of 3 tiles (a chunk's dBias2 strip fits in TMEM next to
 // S/dP, dQ, dK|dV) and reduces dK/dV over the chunks in fp32.
 bool bwd_available(const evo_attn_desc* d) {
-  return d->dtype != EVO_F32 && (d->D == 16 || d->D == 32) && d->L % 8 == 0 && device_supported();
+  return d->dtype != EVO_F32 && (d->D == 8 || d->D == 16 || d->D == 32) && d->L % 8 == 0 && device_supported();
 }
 
 evo_status bwd(EVO_BWD_ARGS) {
   switch (d->D) {
+    case 8:  // zero-padded to the D = 16 kernels (TMA fills the padded columns with zeros)
     case 16: return launch_bwd16(EVO_BWD_PASS);
     case 32: return d->dtype == EVO_F16 ? launch_bwd<32, true>(EVO_BWD_PASS) : launch_bwd<32, false>(EVO_BWD_PASS);
     default: *err = "tcgen05 backward supports D in {16, 32}"; return EVO_ERR_UNSUPPORTED;
@@ -564,6 +573,7 @@ evo_status fwd(const evo_attn_desc* d, const Shape& s, const void* q, const void
                float* lse, void*, cudaStream_t st, int* launches, std::string* err) {
   const bool f16 = d->dtype == EVO_F16;
   switch (d->D) {
+    case 8:  // zero-padded to the D = 16 kernel (TMA fills the padded columns with zeros)
     case 16: return f16 ? launch_fwd<16, true>(d, s, q, k, v, o, lse, st, launches, err)
                         : launch_fwd<16, false>(d, s, q, k, v, o, lse, st, launches, err);
     case 32: return f16 ? launch_fwd<32, true>(d, s, q, k, v, o, lse, st, launches, err)

@@ -79,6 +79,18 @@ def test_head_dims(D):
     check((1, 3, 70, 2, D), "bf16")
 
 
+@pytest.mark.parametrize("shape", [(1, 4, 128, 2, 8), (1, 8, 384, 4, 8), (2, 3, 200, 2, 8), (1, 2, 640, 2, 8)])
+def test_d8_on_tcgen05(shape):
+    # D = 8 (the reference's attn-bench shape family, run.cpp:137-157) runs the D = 16 tcgen05 kernels on
+    # zero-padded TMA boxes: forward and backward (incl. chunked query axis, outer batch)
+    import paper_2310_04610_b200 as E
+
+    check(shape, "bf16", need_dbias1=shape[2] <= 384)
+    q = torch.zeros(shape, dtype=torch.bfloat16, device="cuda")
+    assert E.resolved_path(q) == "tcgen05"
+    assert E.resolved_path(q, direction="bwd") == "tcgen05"
+
+
 def test_fp32_small_d_reference_bench_shape():
     # the reference's attn-bench default (4,130,2,8) F32 (run.cpp:137-157)
     check((1, 4, 130, 2, 8), "f32")

@@ -4,7 +4,7 @@
 set -x
 O=gpurun_out/r02
 mkdir -p $O
-python bench.py --steps 3 --warmup 3 --no-cpu-baseline --no-parity --e2e-steps 2 > $O/bench_pre.json 2>/dev/null
+python bench.py --steps 3 --warmup 3 --no-cpu-baseline --no-parity --e2e-steps 2 > $O/bench_pre.json 2>/dev/null && echo bench ok
 ncu --metrics gpu__time_duration.sum --clock-control none -c 80 --csv --log-file $O/launches_c4.csv \
     python bench.py --steps 3 --warmup 3 --no-cpu-baseline --no-parity --e2e-steps 1 > /dev/null 2>&1
 for cfg in c4 c5 c2 c3; do
@@ -22,3 +22,13 @@ for shp in 1,4,130,2,32 1,4,256,2,32 1,2,640,2,32; do
   done
 done
 ls -la $O
+# summaries on the box (the reports are large): key counters per kernel, traffic merged for bench.py
+for cfg in c4 c5 c2 c3 d8; do
+  python tools/ncu_summarize.py full $O/full_$cfg.ncu-rep $O/r02_ncu_full_$cfg.md --config $cfg \
+      --traffic $O/ncu_traffic.json > /dev/null 2>&1 || echo "summary $cfg failed"
+  ncu -i $O/full_$cfg.ncu-rep --page raw --csv > $O/raw_$cfg.csv 2>/dev/null
+  [ $cfg != c4 ] && rm -f $O/full_$cfg.ncu-rep
+done
+python tools/ncu_summarize.py launches $O/launches_c4.csv $O/r02_launches_c4.md --config c4 > /dev/null 2>&1
+head -c 600 $O/sanitizer_memcheck_1x4x256x2x32.log
+du -sh $O
