@@ -429,7 +429,8 @@ def main():
     traffic = None
     try:
         with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
-            traffic = json.load(f).get(f"{args.config}_{dom_name}_{path}")
+            tj = json.load(f)  # per-call DRAM bytes (the backward call = preamble + main kernel + conversions)
+            traffic = tj.get(f"{args.config}_{dom_name}_call_{path}", tj.get(f"{args.config}_{dom_name}_{path}"))
     except Exception:
         pass
     roofline = {"bound": bound, "achieved": achieved, "peak": peak, "unit": "GB/s" if bound == "hbm" else "TFLOP/s",
