@@ -66,13 +66,13 @@ struct FwdParams {
   uint32_t aug_c;    // (c_lo << 16) | c_hi: 16-bit two-term split of 1/scale
   int b1_rows;       // bias1 rows staged in shared memory per Q slot (b1_tma and the budget allows)
   int* flag;         // numeric-check flag (non-finite LSE / NaN O) or null
-  const void* gate;  // output-gate logits (layout of o) or null: o = sigmoid(gate) * attention
-  int dreal;         // head dim in memory (D = 16 kernels serve D = 8: TMA zero-fills the padded columns)
   const void* bias1;  // [B, L] or null
   const void* bias2;  // [Bo, H, L, L] (read directly in kBiasGlobal mode)
   void* o;           // [B, L, H, D]
   float* lse;        // [B, H, L]
   unsigned long long* trace;  // bring-up timeline of CTA 0 (null in production)
+  const void* gate;  // output-gate logits (layout of o) or null: o = sigmoid(gate) * attention
+  int dreal;         // head dim in memory (D = 16 kernels serve D = 8: TMA zero-fills the padded columns)
 };
 
 enum TraceEv { kTrKV = 0, kTrS = 1, kTrSseen = 2, kTrP0 = 3, kTrP1 = 4, kTrPV = 5, kTrRowEnd = 6, kTrRowStart = 7 };
@@ -150,7 +150,7 @@ __device__ __forceinline__ SegInfo seg_info(long long s0, const FwdParams& p) {
   return si;
 }
 
-template <int D, bool F16, int BM, bool SAFE>  // SAFE: numeric checks compiled in
+template <int D, bool F16, int BM, bool SAFE>  // SAFE: numeric checks, output gate, padded head dim compiled in
 __global__ void __launch_bounds__(FwdCfg<D>::kThreads, 1)
     fwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
                const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmB2,
@@ -599,13 +599,14 @@ __global__ void __launch_bounds__(FwdCfg<D>::kThreads, 1)
         if (tid_wg == 0 && wg == 0) trace(p, kTrRowEnd, tl);
         if (i < p.L) {
           const float inv = l_run > 0.f ? __frcp_rn(l_run) : 0.f;
-          const size_t orow = ((p.swapped ? (size_t)i * p.B + b : (size_t)b * p.L + i) * p.H + si.h) * p.dreal;
+          const int dreal = SAFE ? p.dreal : D;  // special cases (gate, padded D, checks) live in the SAFE variant
+          const size_t orow = ((p.swapped ? (size_t)i * p.B + b : (size_t)b * p.L + i) * p.H + si.h) * dreal;
           uint32_t ow[D / 2];
-          if (p.gate) {  // fused output gate (OpenFold): o = sigmoid(G) * O, G read in the row's layout
+          if (SAFE && p.gate) {  // fused output gate (OpenFold): o = sigmoid(G) * O, G read in the row's layout
             const uint4* g4 = (const uint4*)((const uint16_t*)p.gate + orow);
 #pragma unroll
             for (int c = 0; c < D / 8; ++c) {
-              if (c * 8 >= p.dreal) break;
+              if (c * 8 >= dreal) break;
               const uint4 gr = __ldg(g4 + c);
               const uint32_t gw[4] = {gr.x, gr.y, gr.z, gr.w};
 #pragma unroll
@@ -627,7 +628,7 @@ __global__ void __launch_bounds__(FwdCfg<D>::kThreads, 1)
           uint4* dst = (uint4*)((uint16_t*)p.o + orow);
 #pragma unroll
           for (int v = 0; v < D / 8; ++v)
-            if (v * 8 < p.dreal) dst[v] = make_uint4(ow[4 * v], ow[4 * v + 1], ow[4 * v + 2], ow[4 * v + 3]);
+            if (v * 8 < dreal) dst[v] = make_uint4(ow[4 * v], ow[4 * v + 1], ow[4 * v + 2], ow[4 * v + 3]);
           const float lv = l_run > 0.f ? (m_run + __log2f(l_run)) * kLn2 : -INFINITY;
           p.lse[((size_t)b * p.H + si.h) * p.L + i] = lv;
           if (SAFE && p.flag) {  // NumericError: a NaN input or no finite logit in the row

@@ -196,7 +196,7 @@ evo_status launch_fwd(const evo_attn_desc* d, const Shape& s, const void* q, con
            : p.bias_mode == kBiasGlobal   ? fwd_kernel<D, F16, kBiasGlobal, S>
                                           : fwd_kernel<D, F16, kBiasNone, S>;
   };
-  auto kern = p.flag ? pick(std::true_type{}) : pick(std::false_type{});
+  auto kern = (p.flag || p.gate || s.D != D) ? pick(std::true_type{}) : pick(std::false_type{});
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   // Grid: one CTA per SM. If every (ob, h, q-tile) unit can get >= 4 CTAs, give each unit the same
   // number of CTAs with aligned row ranges (the q-tiles of a row then run concurrently and share
@@ -423,7 +423,7 @@ evo_status launch_bwd(const evo_attn_desc* d, const Shape& s, const void* dout, 
     return s.swapped ? (dkv_reduce ? bk::bwd_kernel<D, F16, true, true, S> : bk::bwd_kernel<D, F16, false, true, S>)
                      : (dkv_reduce ? bk::bwd_kernel<D, F16, true, false, S> : bk::bwd_kernel<D, F16, false, false, S>);
   };
-  auto kern = (det || win || s.flag) ? pick(std::true_type{}) : pick(std::false_type{});
+  auto kern = (det || win || s.flag || s.D != D) ? pick(std::true_type{}) : pick(std::false_type{});
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   const int G = sm_count();
   auto pdl_launch = [&](auto fn, dim3 grid, dim3 block, size_t shm, auto... args) {
