@@ -107,6 +107,12 @@ struct Params {
   uint32_t aug_c;      // (c_lo << 16) | c_hi: 16-bit split of 1/scale
   unsigned long long* trace;  // bring-up timeline of CTA 0 (null in production)
   int swapped;  // 1: q/k/v/o/dO/dQ/dK/dV are [L, B, H, D] (raw msa_col / tri_end layout)
+};
+
+// Fields only the SAFE kernel variants read. They extend the parameter block of those variants alone:
+// the hot variants keep the block they were tuned with (extra fields measurably changed their code
+// generation).
+struct Extra {
   // Row window of this launch: rows n in [n0w, n0w + nw) of every outer batch (items walk the window;
   // the deterministic mode bounds its partial buffers by launching window after window)
   int n0w, nw;
@@ -121,6 +127,20 @@ struct Params {
   int* flag;        // numeric-check flag (NaN dK / dV) or null
   int dreal;        // head dim in memory (D = 16 kernels serve D = 8 with zero-padded TMA boxes)
 };
+struct ParamsSafe : Params {
+  Extra x;
+};
+template <bool SAFE>
+using ParamsT = typename std::conditional<SAFE, ParamsSafe, Params>::type;
+// The extension as the kernel sees it: the launch's values (SAFE) or the constants of a plain launch
+template <bool SAFE, int D>
+__device__ __forceinline__ Extra extra_of(const ParamsT<SAFE>& p) {
+  if constexpr (SAFE) {
+    return p.x;
+  } else {
+    return Extra{0, p.N, 0, 0, nullptr, nullptr, nullptr, D};
+  }
+}
 
 // CTA-0 timeline of steps [kTrFirst, kTrFirst + 64): 8 events x 64 steps (bring-up aid)
 constexpr uint32_t kTrFirst = 100;
@@ -139,12 +159,8 @@ struct Walker {
     return e < t1 ? e : t1;
   }
 };
-// rows walked per unit: the launch's row window (deterministic mode) or all N rows
-template <bool SAFE>
-__device__ __forceinline__ int walk_rows(const Params& p) { return SAFE ? p.nw : p.N; }
-template <bool SAFE>
-__device__ __forceinline__ Walker make_walker(const Params& p) {
-  const int nw = walk_rows<SAFE>(p);
+// nw: rows walked per unit — the launch's row window (SAFE variants) or all N rows
+__device__ __forceinline__ Walker make_walker(const Params& p, int nw) {
   if (p.aligned) {
     const long long unit = blockIdx.x / p.split, part = blockIdx.x % p.split;
     const long long base = unit * nw;
@@ -155,10 +171,8 @@ __device__ __forceinline__ Walker make_walker(const Params& p) {
 struct Unit {
   int ob, h, jt, ic, it0, it1, n0;  // query tiles [it0, it1) of chunk ic
 };
-template <bool SAFE>
-__device__ __forceinline__ Unit unit_of(long long s0, const Params& p) {
+__device__ __forceinline__ Unit unit_of(long long s0, const Params& p, int nw) {
   Unit u;
-  const int nw = walk_rows<SAFE>(p);
   long long x = s0 / nw;
   u.n0 = (int)(s0 - x * nw);  // window-local row
   u.ic = (int)(x % p.nIC);
@@ -184,9 +198,9 @@ __device__ __forceinline__ int ld_acquire(const int* p) {
 }
 // Index of this CTA among the CTAs whose item ranges intersect `unit` (0 = the first): the flush
 // order of the deterministic dBias2 reduction.
-__device__ __forceinline__ int unit_part(const Params& p, long long unit) {
+__device__ __forceinline__ int unit_part(const Params& p, long long unit, int nw) {
   if (p.aligned) return (int)(blockIdx.x % p.split);
-  const long long first = unit * p.nw;  // first item of the unit; CTA c covers [total*c/G, total*(c+1)/G)
+  const long long first = unit * nw;  // first item of the unit; CTA c covers [total*c/G, total*(c+1)/G)
   long long c = first * gridDim.x / p.total;
   while (c > 0 && p.total * c / gridDim.x > first) --c;
   while (p.total * (c + 1) / gridDim.x <= first) ++c;
@@ -228,7 +242,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmdO,
                const __grid_constant__ CUtensorMap tmB2, const __grid_constant__ CUtensorMap tmdQ,
                const __grid_constant__ CUtensorMap tmdK, const __grid_constant__ CUtensorMap tmdV,
-               const Params p) {
+               const ParamsT<SAFE> p) {
   using C = Cfg<D, CH>;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
@@ -268,7 +282,8 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   const int warp = threadIdx.x / 32;
   const int lane = threadIdx.x % 32;
-  const Walker W = make_walker<SAFE>(p);
+  const Extra X = extra_of<SAFE, D>(p);  // compile-time constants in the plain variants
+  const Walker W = make_walker(p, X.nw);
   constexpr uint32_t kSw = ptx::swizzle_code(C::kRowBytes);
 
   if (threadIdx.x == 0) {
@@ -334,7 +349,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       uint32_t bph = 0, pstep = 0;
       for (long long s0 = W.t0; s0 < W.t1; s0 = W.seg_end(s0)) {
         const int cnt = (int)(W.seg_end(s0) - s0);
-        const Unit u = unit_of<SAFE>(s0, p);
+        const Unit u = unit_of(s0, p, X.nw);
         const int plane = u.ob * p.H + u.h;
         if (p.has_bias2) {
           ptx::mbar_wait(bias_empty, bph ^ 1);
@@ -345,7 +360,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         int n = u.n0;
         for (int a = 0; a < cnt; ++a, ++n) {
-          const int b = u.ob * p.N + (SAFE ? p.n0w : 0) + n;
+          const int b = u.ob * p.N + X.n0w + n;
           // K, V (and the bias1 chunk) of this row's key tile
           ptx::mbar_wait(&k_empty[ks], kph ^ 1);
           const int nk = min(kBN, p.L - u.jt * kBN);  // keys of this tile (multiple of 8)
@@ -395,7 +410,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint32_t step = 0, rows = 0;
     for (long long s0 = W.t0; s0 < W.t1; s0 = W.seg_end(s0)) {
       const int cnt = (int)(W.seg_end(s0) - s0);
-      const Unit u = unit_of<SAFE>(s0, p);
+      const Unit u = unit_of(s0, p, X.nw);
       for (int a = 0; a < cnt; ++a) {
         for (int it = (CH ? u.it0 : 0); it < (CH ? u.it1 : p.nQT); ++it) {
           const uint32_t sb = step & 1, ph = (step >> 1) & 1;
@@ -479,7 +494,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint32_t step = 0;
     for (long long s0 = W.t0; s0 < W.t1; s0 = W.seg_end(s0)) {
       const int cnt = (int)(W.seg_end(s0) - s0);
-      const Unit u = unit_of<SAFE>(s0, p);
+      const Unit u = unit_of(s0, p, X.nw);
       for (int a = 0; a < cnt; ++a) {
         ptx::mbar_wait(&k_full[ks], kph);
         if (p.aug) {
@@ -555,7 +570,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint32_t step = 0, bph = 0, uph = 0;
     for (long long s0 = W.t0; s0 < W.t1; s0 = W.seg_end(s0)) {
       const int cnt = (int)(W.seg_end(s0) - s0);
-      const Unit u = unit_of<SAFE>(s0, p);
+      const Unit u = unit_of(s0, p, X.nw);
       if (p.has_bias2) ptx::mbar_wait(bias_full, bph);
       for (int a = 0; a < cnt; ++a) {
         for (int it = (CH ? u.it0 : 0); it < (CH ? u.it1 : p.nQT); ++it) {
@@ -648,11 +663,11 @@ __global__ void __launch_bounds__(kThreads, 1)
         ptx::mbar_wait(strip_full, uph);
         uph ^= 1;
         ptx::tc_fence_after();
-        const long long unit = s0 / p.nw;
-        if (SAFE && p.det) {  // the unit's CTAs flush in part order: wait for the lower parts' warpgroups
-          const int part = unit_part(p, unit);
+        const long long unit = s0 / X.nw;
+        if (SAFE && X.det) {  // the unit's CTAs flush in part order: wait for the lower parts' warpgroups
+          const int part = unit_part(p, unit, X.nw);
           if (tid_wg == 0)
-            while (ld_acquire(p.tickets + unit) < part * kSoftWG) __nanosleep(64);
+            while (ld_acquire(X.tickets + unit) < part * kSoftWG) __nanosleep(64);
           ptx::named_bar_sync(1 + wg, 128);
         }
         const int j0 = u.jt * kBN + (int)col;
@@ -676,10 +691,10 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
         }
       }
-      if (p.dbias2 && SAFE && p.det) {  // this warpgroup's adds are performed before the next part may start
+      if (p.dbias2 && SAFE && X.det) {  // this warpgroup's adds are performed before the next part may start
         __threadfence();
         ptx::named_bar_sync(1 + wg, 128);
-        if (tid_wg == 0) atomicAdd(p.tickets + s0 / p.nw, 1);
+        if (tid_wg == 0) atomicAdd(X.tickets + s0 / X.nw, 1);
       }
       if (p.dbias2) ptx::tc_fence_before();  // strip reads ordered before the next P/dS arrival (its MMAs overwrite)
       if (p.dbias2 && p.dbias2_mc) __threadfence_system();  // remote adds ordered before the ranks' barrier
@@ -699,12 +714,12 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint32_t step = 0, rows = 0;
     for (long long s0 = W.t0; s0 < W.t1; s0 = W.seg_end(s0)) {
       const int cnt = (int)(W.seg_end(s0) - s0);
-      const Unit u = unit_of<SAFE>(s0, p);
+      const Unit u = unit_of(s0, p, X.nw);
       int n = u.n0;
       for (int a = 0; a < cnt; ++a, ++n) {
-        const int b = u.ob * p.N + (SAFE ? p.n0w : 0) + n;
-        const int wrow = u.ob * p.nw + n;  // row of the window (deterministic partial slots)
-        const int Bw = p.Bo * p.nw;
+        const int b = u.ob * p.N + X.n0w + n;
+        const int wrow = u.ob * X.nw + n;  // row of the window (deterministic partial slots)
+        const int Bw = p.Bo * X.nw;
         for (int it = (CH ? u.it0 : 0); it < (CH ? u.it1 : p.nQT); ++it) {
           // ---- dQ partial: TMEM -> staging (fp32, swizzled rows) -> TMA reduce-add into dQacc
           ptx::mbar_wait(dq_full, step & 1);
@@ -732,8 +747,8 @@ __global__ void __launch_bounds__(kThreads, 1)
           ptx::fence_proxy_async_smem();
           ptx::named_bar_sync(kEpiBar, 128);
           if (tid_e == 0) {
-            if (SAFE && p.det) ptx::tma_store_4d(&tmdQ, stg, 0, u.h, it * kBM, u.jt * Bw + wrow);  // key tile jt's slot
-            else ptx::tma_reduce_add_4d(&tmdQ, stg, 0, u.h, it * kBM, (SAFE && p.win) ? wrow : b);
+            if (SAFE && X.det) ptx::tma_store_4d(&tmdQ, stg, 0, u.h, it * kBM, u.jt * Bw + wrow);  // key tile jt's slot
+            else ptx::tma_reduce_add_4d(&tmdQ, stg, 0, u.h, it * kBM, (SAFE && X.win) ? wrow : b);
             ptx::bulk_commit();
             trace(p, kTbDqOut, step);
           }
@@ -753,7 +768,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (p.dbias1 && lane < 16) {  // lanes 0-15 of quadrant q4 hold keys q4*16 + lane (M=64 layout)
           const int jj = u.jt * kBN + q4 * 16 + lane;
           if (jj < p.L) {
-            if (SAFE && p.det) p.db1_part[(((size_t)u.h * p.nIC + u.ic) * Bw + wrow) * p.L + jj] = __uint_as_float(b1v[0]);
+            if (SAFE && X.det) X.db1_part[(((size_t)u.h * p.nIC + u.ic) * Bw + wrow) * p.L + jj] = __uint_as_float(b1v[0]);
             else atomicAdd(p.dbias1 + (size_t)b * p.L + jj, __uint_as_float(b1v[0]));
           }
         }
@@ -777,11 +792,11 @@ __global__ void __launch_bounds__(kThreads, 1)
           ptx::fence_proxy_async_smem();
           ptx::named_bar_sync(kEpiBar, 128);
           if (tid_e == 0) {
-            if (SAFE && p.det) {  // chunk ic's slot
+            if (SAFE && X.det) {  // chunk ic's slot
               ptx::tma_store_4d(&tmdK, stg, 0, u.h, u.jt * kBN, u.ic * Bw + wrow);
               ptx::tma_store_4d(&tmdV, stg + 64 * D, 0, u.h, u.jt * kBN, u.ic * Bw + wrow);
             } else {
-              const int ar = (SAFE && p.win) ? wrow : b;
+              const int ar = (SAFE && X.win) ? wrow : b;
               ptx::tma_reduce_add_4d(&tmdK, stg, 0, u.h, u.jt * kBN, ar);
               ptx::tma_reduce_add_4d(&tmdV, stg + 64 * D, 0, u.h, u.jt * kBN, ar);
             }
@@ -792,11 +807,11 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         const int j = u.jt * kBN + krow;
         if (j < p.L) {
-          if (SAFE && p.flag) {
+          if (SAFE && X.flag) {
             bool nan = false;
 #pragma unroll
             for (int d = 0; d < D; ++d) nan |= isnan(__uint_as_float(v[d]));
-            flag_if(p.flag, nan);
+            flag_if(X.flag, nan);
           }
           const float sc = isk ? p.scale : 1.f;
           uint32_t ow[D / 2];
@@ -805,10 +820,10 @@ __global__ void __launch_bounds__(kThreads, 1)
             ow[d / 2] = F16 ? ptx::pack_f16(__uint_as_float(v[d]) * sc, __uint_as_float(v[d + 1]) * sc)
                             : ptx::pack_bf16(__uint_as_float(v[d]) * sc, __uint_as_float(v[d + 1]) * sc);
           uint4* dst = (uint4*)((uint16_t*)(isk ? p.dk : p.dv) +
-                                   ((SW ? (size_t)j * p.B + b : (size_t)b * p.L + j) * p.H + u.h) * (SAFE ? p.dreal : D));
+                                   ((SW ? (size_t)j * p.B + b : (size_t)b * p.L + j) * p.H + u.h) * X.dreal);
 #pragma unroll
           for (int q = 0; q < D / 8; ++q)
-            if (q * 8 < (SAFE ? p.dreal : D)) dst[q] = make_uint4(ow[4 * q], ow[4 * q + 1], ow[4 * q + 2], ow[4 * q + 3]);
+            if (q * 8 < X.dreal) dst[q] = make_uint4(ow[4 * q], ow[4 * q + 1], ow[4 * q + 2], ow[4 * q + 3]);
         }
       }
     }

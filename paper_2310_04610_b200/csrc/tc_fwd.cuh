@@ -59,7 +59,7 @@ struct FwdParams {
   int aligned;       // 1: CTA c owns part c%split of unit c/split; 0: flat contiguous split
   int split;
   float scale_log2;
-  int bias_mode;
+  int dreal;         // head dim in memory (D = 16 kernels serve D = 8: TMA zero-fills the padded columns)
   int nbias_slots;   // resident: nKT; streamed: 3
   int b1_tma;        // bias1 rows fetched by TMA bulk copy (L % 8 == 0)
   int aug;           // bias1 / key mask enter S as one extra K=16 MMA step (bias1 present or L % 64 != 0)
@@ -70,9 +70,12 @@ struct FwdParams {
   const void* bias2;  // [Bo, H, L, L] (read directly in kBiasGlobal mode)
   void* o;           // [B, L, H, D]
   float* lse;        // [B, H, L]
-  unsigned long long* trace;  // bring-up timeline of CTA 0 (null in production)
-  const void* gate;  // output-gate logits (layout of o) or null: o = sigmoid(gate) * attention
-  int dreal;         // head dim in memory (D = 16 kernels serve D = 8: TMA zero-fills the padded columns)
+  // The parameter block keeps the layout the hot kernel variants were tuned with (extra fields measurably
+  // changed their code generation): the gate pointer shares the slot of the bring-up trace buffer
+  union {
+    unsigned long long* trace;  // bring-up timeline of CTA 0 (EVO_TRACE builds only)
+    const void* gate;           // output-gate logits (layout of o) or null: o = sigmoid(gate) * attention
+  };
 };
 
 enum TraceEv { kTrKV = 0, kTrS = 1, kTrSseen = 2, kTrP0 = 3, kTrP1 = 4, kTrPV = 5, kTrRowEnd = 6, kTrRowStart = 7 };
@@ -599,36 +602,49 @@ __global__ void __launch_bounds__(FwdCfg<D>::kThreads, 1)
         if (tid_wg == 0 && wg == 0) trace(p, kTrRowEnd, tl);
         if (i < p.L) {
           const float inv = l_run > 0.f ? __frcp_rn(l_run) : 0.f;
-          const int dreal = SAFE ? p.dreal : D;  // special cases (gate, padded D, checks) live in the SAFE variant
-          const size_t orow = ((p.swapped ? (size_t)i * p.B + b : (size_t)b * p.L + i) * p.H + si.h) * dreal;
-          uint32_t ow[D / 2];
-          if (SAFE && p.gate) {  // fused output gate (OpenFold): o = sigmoid(G) * O, G read in the row's layout
-            const uint4* g4 = (const uint4*)((const uint16_t*)p.gate + orow);
+          if constexpr (SAFE) {  // special cases (gate, padded D) live in the SAFE variant only
+            const int dreal = p.dreal;
+            const size_t orow = ((p.swapped ? (size_t)i * p.B + b : (size_t)b * p.L + i) * p.H + si.h) * dreal;
+            uint32_t ow[D / 2];
+            if (p.gate) {  // fused output gate (OpenFold): o = sigmoid(G) * O, G read in the row's layout
+              const uint4* g4 = (const uint4*)((const uint16_t*)p.gate + orow);
 #pragma unroll
-            for (int c = 0; c < D / 8; ++c) {
-              if (c * 8 >= dreal) break;
-              const uint4 gr = __ldg(g4 + c);
-              const uint32_t gw[4] = {gr.x, gr.y, gr.z, gr.w};
+              for (int c = 0; c < D / 8; ++c) {
+                if (c * 8 >= dreal) break;
+                const uint4 gr = __ldg(g4 + c);
+                const uint32_t gw[4] = {gr.x, gr.y, gr.z, gr.w};
 #pragma unroll
-              for (int e = 0; e < 4; ++e) {
-                const int d = c * 8 + 2 * e;
-                const float2 g = unpack2<F16>(gw[e]);
-                const float o0 = __uint_as_float(ov[d]) * inv * sigmoidf_fast(g.x);
-                const float o1 = __uint_as_float(ov[d + 1]) * inv * sigmoidf_fast(g.y);
+                for (int e = 0; e < 4; ++e) {
+                  const int d = c * 8 + 2 * e;
+                  const float2 g = unpack2<F16>(gw[e]);
+                  const float o0 = __uint_as_float(ov[d]) * inv * sigmoidf_fast(g.x);
+                  const float o1 = __uint_as_float(ov[d + 1]) * inv * sigmoidf_fast(g.y);
+                  ow[d / 2] = F16 ? ptx::pack_f16(o0, o1) : ptx::pack_bf16(o0, o1);
+                }
+              }
+            } else {
+#pragma unroll
+              for (int d = 0; d < D; d += 2) {
+                const float o0 = __uint_as_float(ov[d]) * inv, o1 = __uint_as_float(ov[d + 1]) * inv;
                 ow[d / 2] = F16 ? ptx::pack_f16(o0, o1) : ptx::pack_bf16(o0, o1);
               }
             }
+            uint4* dst = (uint4*)((uint16_t*)p.o + orow);
+#pragma unroll
+            for (int v = 0; v < D / 8; ++v)
+              if (v * 8 < dreal) dst[v] = make_uint4(ow[4 * v], ow[4 * v + 1], ow[4 * v + 2], ow[4 * v + 3]);
           } else {
+            uint32_t ow[D / 2];
 #pragma unroll
             for (int d = 0; d < D; d += 2) {
               const float o0 = __uint_as_float(ov[d]) * inv, o1 = __uint_as_float(ov[d + 1]) * inv;
               ow[d / 2] = F16 ? ptx::pack_f16(o0, o1) : ptx::pack_bf16(o0, o1);
             }
-          }
-          uint4* dst = (uint4*)((uint16_t*)p.o + orow);
+            uint4* dst = (uint4*)((uint16_t*)p.o +
+                                   ((p.swapped ? (size_t)i * p.B + b : (size_t)b * p.L + i) * p.H + si.h) * D);
 #pragma unroll
-          for (int v = 0; v < D / 8; ++v)
-            if (v * 8 < dreal) dst[v] = make_uint4(ow[4 * v], ow[4 * v + 1], ow[4 * v + 2], ow[4 * v + 3]);
+            for (int v = 0; v < D / 8; ++v) dst[v] = make_uint4(ow[4 * v], ow[4 * v + 1], ow[4 * v + 2], ow[4 * v + 3]);
+          }
           const float lv = l_run > 0.f ? (m_run + __log2f(l_run)) * kLn2 : -INFINITY;
           p.lse[((size_t)b * p.H + si.h) * p.L + i] = lv;
           if (SAFE && p.flag) {  // NumericError: a NaN input or no finite logit in the row

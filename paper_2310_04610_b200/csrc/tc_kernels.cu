@@ -148,6 +148,7 @@ evo_status launch_fwd(const evo_attn_desc* d, const Shape& s, const void* q, con
       !map_bl_hd(&tv, v, s, kBN, dt, 2, err, false, D))
     return EVO_ERR_CUDA;
   FwdParams p{};
+  int bias_mode = kBiasNone;
   p.B = s.B; p.N = s.N; p.L = s.L; p.H = s.H; p.Bo = (int)d->Bo;
   p.swapped = s.swapped;
   p.nQT = (s.L + kBM - 1) / kBM;
@@ -157,11 +158,17 @@ evo_status launch_fwd(const evo_attn_desc* d, const Shape& s, const void* q, con
   p.bias1 = s.bias1;
   p.bias2 = s.bias2;
   p.o = o;
-  p.gate = s.gate;
   p.dreal = s.D;
   p.lse = lse;
-  p.trace = g_trace;
-  p.bias_mode = kBiasNone;
+  if (s.gate) {  // the gate pointer shares its slot with the bring-up trace buffer
+    if (EVO_TRACE) {
+      *err = "the output gate is not available in EVO_TRACE bring-up builds";
+      return EVO_ERR_UNSUPPORTED;
+    }
+    p.gate = s.gate;
+  } else {
+    p.trace = g_trace;
+  }
   p.nbias_slots = 0;
   p.b1_tma = (s.L % 8 == 0) ? 1 : 0;
   p.aug = (s.bias1 != nullptr || s.L % kBN != 0) ? 1 : 0;
@@ -172,14 +179,14 @@ evo_status launch_fwd(const evo_attn_desc* d, const Shape& s, const void* q, con
   p.b1_rows = (s.bias1 && p.b1_tma && fwd_smem_bytes<D>(3, p.nKT, true) <= kMaxSmem) ? 1 : 0;
   if (s.bias2) {
     if (s.L % 8 != 0) {
-      p.bias_mode = kBiasGlobal;
+      bias_mode = kBiasGlobal;
     } else {
       if (!map_bias(&tb, s.bias2, s, p.Bo, dt, err)) return EVO_ERR_CUDA;
       if (fwd_smem_bytes<D>(p.nKT, p.nKT, p.b1_rows) <= kMaxSmem) {
-        p.bias_mode = kBiasResident;
+        bias_mode = kBiasResident;
         p.nbias_slots = p.nKT;
       } else {
-        p.bias_mode = kBiasStreamed;
+        bias_mode = kBiasStreamed;
         p.nbias_slots = 3;
       }
     }
@@ -191,12 +198,12 @@ evo_status launch_fwd(const evo_attn_desc* d, const Shape& s, const void* q, con
   }
   auto pick = [&](auto safe) {
     constexpr bool S = decltype(safe)::value;
-    return p.bias_mode == kBiasResident   ? fwd_kernel<D, F16, kBiasResident, S>
-           : p.bias_mode == kBiasStreamed ? fwd_kernel<D, F16, kBiasStreamed, S>
-           : p.bias_mode == kBiasGlobal   ? fwd_kernel<D, F16, kBiasGlobal, S>
+    return bias_mode == kBiasResident   ? fwd_kernel<D, F16, kBiasResident, S>
+           : bias_mode == kBiasStreamed ? fwd_kernel<D, F16, kBiasStreamed, S>
+           : bias_mode == kBiasGlobal   ? fwd_kernel<D, F16, kBiasGlobal, S>
                                           : fwd_kernel<D, F16, kBiasNone, S>;
   };
-  auto kern = (p.flag || p.gate || s.D != D) ? pick(std::true_type{}) : pick(std::false_type{});
+  auto kern = (p.flag || s.gate || s.D != D) ? pick(std::true_type{}) : pick(std::false_type{});
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   // Grid: one CTA per SM. If every (ob, h, q-tile) unit can get >= 4 CTAs, give each unit the same
   // number of CTAs with aligned row ranges (the q-tiles of a row then run concurrently and share
@@ -361,7 +368,7 @@ evo_status launch_bwd(const evo_attn_desc* d, const Shape& s, const void* dout, 
             : map_bl_hd(&tdq, dqacc, s, bk::kBM, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, err, true, D)))
     return EVO_ERR_CUDA;
   if (s.bias2 && !map_bias(&tb, s.bias2, s, (int)d->Bo, dt, err)) return EVO_ERR_CUDA;
-  bk::Params p{};
+  bk::ParamsSafe p{};  // the plain variants get its base (bk::Params) slice
   p.B = s.B; p.N = s.N; p.L = s.L; p.H = s.H; p.Bo = (int)d->Bo;
   p.swapped = s.swapped;
   p.nQT = (s.L + bk::kBM - 1) / bk::kBM;
@@ -384,11 +391,11 @@ evo_status launch_bwd(const evo_attn_desc* d, const Shape& s, const void* dout, 
   }
   p.has_bias2 = s.bias2 != nullptr;
   p.trace = g_trace_bwd;
-  p.det = det ? 1 : 0;
-  p.win = win ? 1 : 0;
-  p.dreal = s.D;
-  p.db1_part = (float*)(ws + w.db1p);
-  p.flag = s.flag;
+  p.x.det = det ? 1 : 0;
+  p.x.win = win ? 1 : 0;
+  p.x.dreal = s.D;
+  p.x.db1_part = (float*)(ws + w.db1p);
+  p.x.flag = s.flag;
   // bias1 (and the key mask past L) enter S through one extra K=16 MMA step: A_aug rows hold a
   // 16-bit two-term split of 1/scale, B_aug rows the bias1 value of each key.
   p.aug = (s.bias1 != nullptr || s.L % bk::kBN != 0) ? 1 : 0;
@@ -418,13 +425,14 @@ evo_status launch_bwd(const evo_attn_desc* d, const Shape& s, const void* dout, 
         (const T*)s.gate, (T*)s.dog, (T*)s.dgate);
   }
   ++*launches;
-  auto pick = [&](auto safe) {
-    constexpr bool S = decltype(safe)::value;
+  const bool safe = det || win || s.flag || s.D != D;
+  auto kern_of = [&](auto sf) {
+    constexpr bool S = decltype(sf)::value;
     return s.swapped ? (dkv_reduce ? bk::bwd_kernel<D, F16, true, true, S> : bk::bwd_kernel<D, F16, false, true, S>)
                      : (dkv_reduce ? bk::bwd_kernel<D, F16, true, false, S> : bk::bwd_kernel<D, F16, false, false, S>);
   };
-  auto kern = (det || win || s.flag || s.D != D) ? pick(std::true_type{}) : pick(std::false_type{});
-  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaFuncSetAttribute(safe ? (const void*)kern_of(std::true_type{}) : (const void*)kern_of(std::false_type{}),
+                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   const int G = sm_count();
   auto pdl_launch = [&](auto fn, dim3 grid, dim3 block, size_t shm, auto... args) {
     cudaLaunchConfig_t cfg = {};  // programmatic dependent launch: the prologue overlaps the predecessor's tail
@@ -443,26 +451,31 @@ evo_status launch_bwd(const evo_attn_desc* d, const Shape& s, const void* dout, 
   const long long units = (long long)p.Bo * p.H * p.nKT * p.nIC;
   const int HD = s.H * s.D;
   for (int wi = 0; wi < w.nwin; ++wi) {
-    p.n0w = wi * w.nw;
-    p.nw = std::min<int>(w.nw, s.N - p.n0w);
-    p.total = units * p.nw;
-    p.tickets = det ? (int*)(ws + w.tickets) + (size_t)wi * units : nullptr;
+    p.x.n0w = wi * w.nw;
+    p.x.nw = std::min<int>(w.nw, s.N - p.x.n0w);
+    p.total = units * p.x.nw;
+    p.x.tickets = det ? (int*)(ws + w.tickets) + (size_t)wi * units : nullptr;
     long long grid = std::min<long long>(p.total, G);
     p.aligned = 0;
     p.split = 1;
     if (units <= G) {
-      p.split = (int)std::min<long long>(G / units, p.nw);
+      p.split = (int)std::min<long long>(G / units, p.x.nw);
       p.aligned = 1;
       grid = units * p.split;
     }
-    pdl_launch(kern, dim3((unsigned)grid), dim3(bk::kThreads), smem, tq, tk, tv, tdo, tb, tdq, tdk, tdv, p);
+    if (safe)
+      pdl_launch(kern_of(std::true_type{}), dim3((unsigned)grid), dim3(bk::kThreads), smem, tq, tk, tv, tdo, tb, tdq,
+                 tdk, tdv, p);
+    else
+      pdl_launch(kern_of(std::false_type{}), dim3((unsigned)grid), dim3(bk::kThreads), smem, tq, tk, tv, tdo, tb, tdq,
+                 tdk, tdv, static_cast<const bk::Params&>(p));
     if (det) {
       // ordered sums of this window's partial slots (dQ over key tiles; dK / dV over query chunks)
-      const size_t n = (size_t)p.Bo * p.nw * s.L * HD, pstride = n;
+      const size_t n = (size_t)p.Bo * p.x.nw * s.L * HD, pstride = n;
       const unsigned cg = (unsigned)std::min<size_t>((n / 8 + 255) / 256, 148 * 16);
       auto conv = [&](float* part, int np, void* out, float scale) {
         pdl_launch(s.swapped ? bk::det_convert_kernel<T, true> : bk::det_convert_kernel<T, false>, dim3(cg), dim3(256),
-                   0, (const float*)part, np, pstride, (T*)out, n, scale, s.B, s.L, HD, s.N, p.n0w, p.nw, s.flag, 0);
+                   0, (const float*)part, np, pstride, (T*)out, n, scale, s.B, s.L, HD, s.N, p.x.n0w, p.x.nw, s.flag, 0);
       };
       conv(dqacc, nkt, dq, s.scale);
       if (dkv_reduce) {
@@ -472,11 +485,11 @@ evo_status launch_bwd(const evo_attn_desc* d, const Shape& s, const void* dout, 
     } else if (win) {
       // this window's accumulators into their rows (the streaming conversion, per outer batch: the rows
       // of one window and outer batch are contiguous), then zeroed for the next window
-      const size_t rowlen = (size_t)s.L * HD, nob = (size_t)p.nw * rowlen;
+      const size_t rowlen = (size_t)s.L * HD, nob = (size_t)p.x.nw * rowlen;
       const unsigned cg = (unsigned)std::min<size_t>((nob / 8 + 255) / 256, 148 * 16);
       auto conv = [&](const float* acc, void* out, float scale) {
         for (int ob = 0; ob < p.Bo; ++ob) {
-          const size_t shift = s.swapped ? (size_t)p.n0w * HD : ((size_t)ob * s.N + p.n0w) * rowlen;
+          const size_t shift = s.swapped ? (size_t)p.x.n0w * HD : ((size_t)ob * s.N + p.x.n0w) * rowlen;
           pdl_launch(s.swapped ? bk::dq_convert_kernel<T, true> : bk::dq_convert_kernel<T, false>, dim3(cg), dim3(256),
                      0, acc + ob * nob, (T*)out + shift, nob, scale, s.B, s.L, HD, s.flag);
         }
@@ -490,10 +503,10 @@ evo_status launch_bwd(const evo_attn_desc* d, const Shape& s, const void* dout, 
     }
     if (det) {
       if (dbias1) {  // dBias1 partials of (head, chunk) slots in order, per outer batch of the window
-        const size_t nl = (size_t)p.nw * s.L;
+        const size_t nl = (size_t)p.x.nw * s.L;
         for (int ob = 0; ob < p.Bo; ++ob) {
           ordered_sum_kernel<float><<<(unsigned)std::min<size_t>((nl + 255) / 256, 148 * 4), 256, 0, st>>>(
-              p.db1_part + (size_t)ob * nl, s.H * nic, (size_t)p.Bo * nl, dbias1 + ((size_t)ob * s.N + p.n0w) * s.L, nl);
+              p.x.db1_part + (size_t)ob * nl, s.H * nic, (size_t)p.Bo * nl, dbias1 + ((size_t)ob * s.N + p.x.n0w) * s.L, nl);
           ++*launches;
         }
       }
