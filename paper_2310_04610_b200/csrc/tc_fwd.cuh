@@ -36,6 +36,9 @@ constexpr float kRescaleThreshold = 8.f;  // log2 units
 #define EVO_FWD_POLY_EVERY 4
 #endif
 constexpr int kPolyEvery = EVO_FWD_POLY_EVERY;  // 1 pair in kPolyEvery exponentiated by polynomial (0: none)
+#ifndef EVO_FWD_SELF_PV
+#define EVO_FWD_SELF_PV 1  // the softmax warpgroup's last thread to finish P issues the PV UMMA itself
+#endif
 
 template <int D>
 struct FwdCfg {
@@ -98,6 +101,11 @@ __device__ __forceinline__ float2 unpack2(uint32_t w) {  // two packed 16-bit fl
   } else {
     return make_float2(__uint_as_float(w << 16), __uint_as_float(w & 0xFFFF0000u));
   }
+}
+__device__ __forceinline__ uint32_t atom_add_acq_rel(uint32_t* a, uint32_t v) {
+  uint32_t old;
+  asm volatile("atom.acq_rel.cta.shared::cta.add.u32 %0, [%1], %2;" : "=r"(old) : "r"(ptx::smem_u32(a)), "r"(v) : "memory");
+  return old;
 }
 __device__ __forceinline__ float fmax3(float a, float b, float c) {
   float d;
@@ -184,6 +192,7 @@ __global__ void __launch_bounds__(FwdCfg<D>::kThreads, 1)
   uint64_t* bias_full = v_empty + C::kStages;    // [nbias_slots]
   uint64_t* bias_empty = bias_full + p.nbias_slots;
   uint32_t* tmem_slot = (uint32_t*)(bias_empty + p.nbias_slots);
+  uint32_t* p_count = tmem_slot + 1;  // [NWG] threads done writing P (self-issued PV: the 128th issues it)
 
   const int warp = threadIdx.x / 32;
   const int lane = threadIdx.x % 32;
@@ -197,7 +206,10 @@ __global__ void __launch_bounds__(FwdCfg<D>::kThreads, 1)
       ptx::mbar_init(&s_free[s], 1);
       ptx::mbar_init(&p_full[s], 128);
     }
-    for (int w = 0; w < NWG; ++w) ptx::mbar_init(&o_free[w], 128);
+    for (int w = 0; w < NWG; ++w) {
+      ptx::mbar_init(&o_free[w], 128);
+      p_count[w] = 0;
+    }
     for (int s = 0; s < C::kStages; ++s) {
       ptx::mbar_init(&kv_full[s], 1);
       ptx::mbar_init(&kv_empty[s], 1);
@@ -424,9 +436,9 @@ __global__ void __launch_bounds__(FwdCfg<D>::kThreads, 1)
               if (j == p.nKT - 1) ptx::tc_commit(&q_empty[w * 2 + qs]);
             }
             __syncwarp();
-            if (j > 0) do_pv(t - 1, j == 1);
+            if (!EVO_FWD_SELF_PV && j > 0) do_pv(t - 1, j == 1);
           }
-          do_pv(t - 1, p.nKT == 1);
+          if (!EVO_FWD_SELF_PV) do_pv(t - 1, p.nKT == 1);
           ++qc;
         }
       }
@@ -585,7 +597,29 @@ __global__ void __launch_bounds__(FwdCfg<D>::kThreads, 1)
           l_run += s01.x + s01.y;
           ptx::tmem_st_wait();
           ptx::tc_fence_before();
-          ptx::mbar_arrive(&p_full[wg * 2 + sb]);
+          if (EVO_FWD_SELF_PV) {
+            // PV(t) = P(t) V_t issued by the warpgroup's last thread to finish writing P (acq_rel
+            // counter: every thread's TMEM stores are ordered before it) — no round trip through the
+            // UMMA warp, which shares its SMSP with three busy softmax warps
+            if ((atom_add_acq_rel(&p_count[wg], 1u) & 127u) == 127u) {
+              ptx::tc_fence_after();
+              const int ks = wg * 2 + (int)(tcount & 1);
+              ptx::mbar_wait(&v_full[ks], (tcount >> 1) & 1);
+              const uint32_t vbase = ptx::smem_u32(sV + ks * C::kTileKV);
+              const uint32_t idO = ptx::instr_desc(kBM, D, F16, false, true);
+              const uint32_t wbase = tmem + wg * C::kWGcols;
+#pragma unroll
+              for (int kk = 0; kk < kBN / 16; ++kk) {
+                const uint64_t bd =
+                    ptx::smem_desc(vbase + kk * 16 * C::kRowBytes, 16 * C::kRowBytes, 8 * C::kRowBytes, kSw);
+                ptx::mma_ts(wbase + 128, wbase + sb * 64 + kk * 8, bd, idO, (j > 0 || kk > 0) ? 1u : 0u);
+              }
+              ptx::tc_commit(&s_free[wg * 2 + sb]);
+              ptx::tc_commit(&v_empty[ks]);
+            }
+          } else {
+            ptx::mbar_arrive(&p_full[wg * 2 + sb]);
+          }
           if (tid_wg == 0) trace(p, wg == 0 ? kTrP0 : kTrP1, tcount);
           ++tcount;
         }
@@ -598,7 +632,7 @@ __global__ void __launch_bounds__(FwdCfg<D>::kThreads, 1)
         for (int c0 = 0; c0 < D; c0 += 16) ptx::tmem_ld16(o_tmem + c0, *(uint32_t(*)[16])(&ov[c0]));
         ptx::tmem_ld_wait();
         ptx::tc_fence_before();
-        ptx::mbar_arrive(&o_free[wg]);
+        if (!EVO_FWD_SELF_PV) ptx::mbar_arrive(&o_free[wg]);
         if (tid_wg == 0 && wg == 0) trace(p, kTrRowEnd, tl);
         if (i < p.L) {
           const float inv = l_run > 0.f ? __frcp_rn(l_run) : 0.f;
