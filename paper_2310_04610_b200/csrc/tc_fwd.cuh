@@ -37,7 +37,7 @@ constexpr float kRescaleThreshold = 8.f;  // log2 units
 #endif
 constexpr int kPolyEvery = EVO_FWD_POLY_EVERY;  // 1 pair in kPolyEvery exponentiated by polynomial (0: none)
 #ifndef EVO_FWD_SELF_PV
-#define EVO_FWD_SELF_PV 1  // the softmax warpgroup's last thread to finish P issues the PV UMMA itself
+#define EVO_FWD_SELF_PV 0  // 1: the softmax warpgroup's last thread to finish P issues the PV UMMA itself
 #endif
 
 template <int D>
@@ -192,7 +192,10 @@ __global__ void __launch_bounds__(FwdCfg<D>::kThreads, 1)
   uint64_t* bias_full = v_empty + C::kStages;    // [nbias_slots]
   uint64_t* bias_empty = bias_full + p.nbias_slots;
   uint32_t* tmem_slot = (uint32_t*)(bias_empty + p.nbias_slots);
-  uint32_t* p_count = tmem_slot + 1;  // [NWG] threads done writing P (self-issued PV: the 128th issues it)
+  // [NWG][2] threads done writing P into S buffer sb (self-issued PV: the 128th issues it). Per buffer: a
+  // thread can run one tile ahead of its warpgroup (the other S buffer), never two (that buffer's S
+  // waits for this PV)
+  uint32_t* p_count = tmem_slot + 1;
 
   const int warp = threadIdx.x / 32;
   const int lane = threadIdx.x % 32;
@@ -208,7 +211,7 @@ __global__ void __launch_bounds__(FwdCfg<D>::kThreads, 1)
     }
     for (int w = 0; w < NWG; ++w) {
       ptx::mbar_init(&o_free[w], 128);
-      p_count[w] = 0;
+      p_count[2 * w] = p_count[2 * w + 1] = 0;
     }
     for (int s = 0; s < C::kStages; ++s) {
       ptx::mbar_init(&kv_full[s], 1);
@@ -601,7 +604,7 @@ __global__ void __launch_bounds__(FwdCfg<D>::kThreads, 1)
             // PV(t) = P(t) V_t issued by the warpgroup's last thread to finish writing P (acq_rel
             // counter: every thread's TMEM stores are ordered before it) — no round trip through the
             // UMMA warp, which shares its SMSP with three busy softmax warps
-            if ((atom_add_acq_rel(&p_count[wg], 1u) & 127u) == 127u) {
+            if ((atom_add_acq_rel(&p_count[wg * 2 + sb], 1u) & 127u) == 127u) {
               ptx::tc_fence_after();
               const int ks = wg * 2 + (int)(tcount & 1);
               ptx::mbar_wait(&v_full[ks], (tcount >> 1) & 1);
@@ -617,6 +620,7 @@ __global__ void __launch_bounds__(FwdCfg<D>::kThreads, 1)
               ptx::tc_commit(&s_free[wg * 2 + sb]);
               ptx::tc_commit(&v_empty[ks]);
             }
+            __syncwarp();  // reconverge before the next .sync.aligned tcgen05 load
           } else {
             ptx::mbar_arrive(&p_full[wg * 2 + sb]);
           }

@@ -113,7 +113,7 @@ size_t fwd_smem_bytes(int nbias_slots, int nKT, bool b1_rows) {
   b += (size_t)nbias_slots * C::kBiasTile;
   b += (size_t)kAugA + (size_t)C::kStages * kAugB;  // bias1 augmentation tiles
   if (b1_rows) b += (size_t)C::NWG * 2 * LP * 2;  // bias1 rows (raw), double buffered per WG
-  b += (size_t)(11 * C::NWG + 4 * C::kStages + 2 * nbias_slots) * 8 + 16 + 4 * C::NWG;
+  b += (size_t)(11 * C::NWG + 4 * C::kStages + 2 * nbias_slots) * 8 + 16 + 8 * C::NWG;
   return b;
 }
 
