@@ -37,13 +37,22 @@ namespace bk {
 constexpr int kBM = 128;   // queries per tile
 constexpr int kBN = 64;    // keys per tile
 // warps: 0 TMA producer, 1 gradient MMAs, 2 S/dP MMAs, 3..3+4*kSoftWG softmax warpgroups, then the epilogue WG
-constexpr int kSoftWG = 4;                              // softmax warpgroups, 16 keys each
+#ifndef EVO_BWD_SOFTWG
+#define EVO_BWD_SOFTWG 4  // softmax warpgroups (fewer warpgroups: more registers per thread)
+#endif
+#ifndef EVO_BWD_UNROLL
+#define EVO_BWD_UNROLL 1  // 1: a warpgroup's 16-key blocks of a step fully unrolled (loads of all blocks in flight)
+#endif
+constexpr int kSoftWG = EVO_BWD_SOFTWG;
 constexpr int kKeysPerThread = 64 / kSoftWG;
 // kGroups groups of softmax warpgroups take turns on the steps (step % kGroups): a group's warpgroup
 // covers kGroups 16-key blocks of its step, so one group's TMEM / shared-memory phases overlap the
 // other's exponentials instead of all warpgroups running the same phase at once
 constexpr int kGroups = EVO_BWD_ALT == 2 ? 4 : EVO_BWD_ALT ? 2 : 1;
 constexpr int kGroupThreads = 128 * kSoftWG / kGroups;
+constexpr int kBlocksPerWG = 4 * kGroups / kSoftWG;  // 16-key blocks a warpgroup covers in each of its steps
+constexpr int kCbUnroll = EVO_BWD_UNROLL ? kBlocksPerWG : 1;
+static_assert(kBlocksPerWG >= 1 && kBlocksPerWG * kSoftWG == 4 * kGroups, "softmax warpgroup / group split");
 constexpr int kSoftWarp0 = 3;
 constexpr int kEpiWarp0 = kSoftWarp0 + 4 * kSoftWG;
 constexpr int kThreads = (kEpiWarp0 + 4) * 32;
@@ -592,9 +601,9 @@ __global__ void __launch_bounds__(kThreads, 1)
           const uint32_t bt = ptx::smem_u32(sBias + (size_t)(it - (CH ? u.it0 : 0)) * C::kBiasTile) + r * 128;
           const uint32_t pbase = ptx::smem_u32(sP + sb * C::kPdsTile) + r * 128;
           const uint32_t dbase = ptx::smem_u32(sdS + sb * C::kPdsTile) + r * 128;
-#pragma unroll 1
-          for (int cb = 0; cb < kGroups; ++cb) {
-            const int kb = sub * kGroups + cb;  // 16-key block of the step
+#pragma unroll(kCbUnroll)
+          for (int cb = 0; cb < kBlocksPerWG; ++cb) {
+            const int kb = sub * kBlocksPerWG + cb;  // 16-key block of the step
             const uint32_t col = (uint32_t)(kb * 16);
             // all loads of the block in flight together: S, dP (TMEM) and the bias2 row (smem)
             uint32_t sv[16], dp[16];
@@ -606,7 +615,7 @@ __global__ void __launch_bounds__(kThreads, 1)
               braw[1] = lds128(bt + ((uint32_t)((2 * kb + 1) << 4) ^ r7));
             }
             ptx::tmem_ld_wait();
-            if (!EVO_BWD_DS_TMEM && cb == kGroups - 1) {
+            if (!EVO_BWD_DS_TMEM && cb == kBlocksPerWG - 1) {
               ptx::tc_fence_before();
               ptx::mbar_arrive(&s_free[sb]);  // S/dP buffer may be recomputed
             }
@@ -670,11 +679,13 @@ __global__ void __launch_bounds__(kThreads, 1)
             while (ld_acquire(X.tickets + unit) < part * kSoftWG) __nanosleep(64);
           ptx::named_bar_sync(1 + wg, 128);
         }
-        const int j0 = u.jt * kBN + (int)col;
-        for (int it = (CH ? u.it0 : 0); it < (CH ? u.it1 : p.nQT); ++it) {
+        for (int it = (CH ? u.it0 : 0); it < (CH ? u.it1 : p.nQT); ++it)
+#pragma unroll
+        for (int c16 = 0; c16 < kKeysPerThread; c16 += 16) {  // 16-column chunks of this warpgroup's strip
+          const int j0 = u.jt * kBN + (int)col + c16;
           const int i = it * kBM + r;
           uint32_t st[16];
-          ptx::tmem_ld16(tmem + lane_off + kStripCol + (it - (CH ? u.it0 : 0)) * 64 + col, st);
+          ptx::tmem_ld16(tmem + lane_off + kStripCol + (it - (CH ? u.it0 : 0)) * 64 + col + c16, st);
           ptx::tmem_ld_wait();
           if (i < p.L) {
             float* dst = p.dbias2 + (((size_t)u.ob * p.H + u.h) * p.L + i) * p.L + j0;
