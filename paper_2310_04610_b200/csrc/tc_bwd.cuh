@@ -37,6 +37,12 @@ namespace bk {
 constexpr int kBM = 128;   // queries per tile
 constexpr int kBN = 64;    // keys per tile
 // warps: 0 TMA producer, 1 gradient MMAs, 2 S/dP MMAs, 3..3+4*kSoftWG softmax warpgroups, then the epilogue WG
+#ifndef EVO_BWD_QSTAGES
+#define EVO_BWD_QSTAGES 4  // (Q, dO, lse, delta) ring depth of the unchunked variants
+#endif
+#ifndef EVO_BWD_PREFETCH
+#define EVO_BWD_PREFETCH 0  // L2 prefetch of the next row's K / V / Q / dO / lse / delta by the producer
+#endif
 #ifndef EVO_BWD_SOFTWG
 #define EVO_BWD_SOFTWG 4  // softmax warpgroups (fewer warpgroups: more registers per thread)
 #endif
@@ -74,7 +80,8 @@ constexpr uint32_t kDb1Col = 384;
 #endif
 #ifndef EVO_BWD_EXP
 #define EVO_BWD_EXP 0  // timing experiments only (wrong results), bit mask: 1 no dK/dV MMAs, 2 no dQ MMA, 4 no bias LDS,
-                       // 8 no P/dS stores, 16 no exponentials, 32 no dQ staging/reduce, 64 no dBias2 strip MMAs
+                       // 8 no P/dS stores, 16 no exponentials, 32 no dQ staging/reduce, 64 no dBias2 strip MMAs,
+                       // 128 every row loads the Q / dO / lse / delta of row 0 (L2-resident)
 #endif  // dBias1 column sums (M=64, 16 columns) when requested: chunks of <= 2 q-tiles
 
 template <int D, bool CH>
@@ -86,8 +93,8 @@ struct Cfg {
   // depth is the TMA slack. 4 deep with one fp32 dQ staging tile (C4: 574 vs 651 us at 3 deep); the
   // chunked variant stages dK/dV partials through the same tiles, and there two staging tiles with a
   // 3-deep ring win (C5: 44.8 vs 57.6 ms)
-  static constexpr int kQStages = CH ? 3 : 4;
-  static constexpr int kDqBufs = kQStages > 3 ? 1 : 2;  // fp32 dQ staging tiles (shared-memory budget)
+  static constexpr int kQStages = CH ? 3 : EVO_BWD_QSTAGES;
+  static constexpr int kDqBufs = (EVO_BWD_EXP & 32) && !CH ? 0 : kQStages > 3 ? 1 : 2;  // fp32 dQ staging tiles
   static constexpr int kKStages = 2;                // (K, V, bias1 chunk) ring
   static constexpr int kBiasTile = kBM * kBN * 2;   // 16 KB
   static constexpr int kPdsTile = kBM * kBN * 2;    // 16 KB (P or dS, bf16)
@@ -370,6 +377,21 @@ __global__ void __launch_bounds__(kThreads, 1)
         int n = u.n0;
         for (int a = 0; a < cnt; ++a, ++n) {
           const int b = u.ob * p.N + X.n0w + n;
+          if (EVO_BWD_PREFETCH && a + 1 < cnt) {
+            // the next row's operands into L2 one row (nQT steps) ahead: its Q-stage loads are issued
+            // only when the gradient MMAs of step - kQStages complete, and then sit on the S -> softmax
+            // chain; from L2 they land in about half the HBM latency
+            ptx::tma_prefetch_4d(&tmK, 0, u.h, u.jt * kBN, b + 1);
+            ptx::tma_prefetch_4d(&tmV, 0, u.h, u.jt * kBN, b + 1);
+            for (int it = (CH ? u.it0 : 0); it < (CH ? u.it1 : p.nQT); ++it) {
+              ptx::tma_prefetch_4d(&tmQ, 0, u.h, it * kBM, b + 1);
+              ptx::tma_prefetch_4d(&tmdO, 0, u.h, it * kBM, b + 1);
+            }
+            const size_t r1 = ((size_t)(b + 1) * p.H + u.h) * (p.nQT * kBM) + (size_t)(CH ? u.it0 : 0) * kBM;
+            const uint32_t nb = (uint32_t)((CH ? u.it1 - u.it0 : p.nQT) * kBM * 4);
+            ptx::bulk_prefetch_l2(p.lse2 + r1, nb);
+            ptx::bulk_prefetch_l2(p.delta + r1, nb);
+          }
           // K, V (and the bias1 chunk) of this row's key tile
           ptx::mbar_wait(&k_empty[ks], kph ^ 1);
           const int nk = min(kBN, p.L - u.jt * kBN);  // keys of this tile (multiple of 8)
@@ -385,9 +407,10 @@ __global__ void __launch_bounds__(kThreads, 1)
             ptx::mbar_wait(&q_empty[qs], qph ^ 1);
             trace(p, kTbProdQ, pstep++);
             ptx::mbar_expect_tx(&q_full[qs], 2 * C::kTileQ + 2 * kBM * 4);
-            ptx::tma_load_4d(sQ + qs * C::kTileQ, &tmQ, &q_full[qs], 0, u.h, it * kBM, b);
-            ptx::tma_load_4d(sdO + qs * C::kTileQ, &tmdO, &q_full[qs], 0, u.h, it * kBM, b);
-            const size_t row0 = ((size_t)b * p.H + u.h) * (p.nQT * kBM) + (size_t)it * kBM;
+            const int bq = (EVO_BWD_EXP & 128) ? 0 : b;
+            ptx::tma_load_4d(sQ + qs * C::kTileQ, &tmQ, &q_full[qs], 0, u.h, it * kBM, bq);
+            ptx::tma_load_4d(sdO + qs * C::kTileQ, &tmdO, &q_full[qs], 0, u.h, it * kBM, bq);
+            const size_t row0 = ((size_t)bq * p.H + u.h) * (p.nQT * kBM) + (size_t)it * kBM;
             bulk_g2s(ptx::smem_u32(sLse + qs * kBM), p.lse2 + row0, kBM * 4, &q_full[qs]);
             bulk_g2s(ptx::smem_u32(sDel + qs * kBM), p.delta + row0, kBM * 4, &q_full[qs]);
             if (++qs == C::kQStages) { qs = 0; qph ^= 1; }
