@@ -853,11 +853,9 @@ __global__ void __launch_bounds__(kThreads, 1)
           for (int d = 0; d < D; d += 2)
             ow[d / 2] = F16 ? ptx::pack_f16(__uint_as_float(v[d]) * sc, __uint_as_float(v[d + 1]) * sc)
                             : ptx::pack_bf16(__uint_as_float(v[d]) * sc, __uint_as_float(v[d + 1]) * sc);
-          uint4* dst = (uint4*)((uint16_t*)(isk ? p.dk : p.dv) +
-                                   ((SW ? (size_t)j * p.B + b : (size_t)b * p.L + j) * p.H + u.h) * X.dreal);
-#pragma unroll
-          for (int q = 0; q < D / 8; ++q)
-            if (q * 8 < X.dreal) dst[q] = make_uint4(ow[4 * q], ow[4 * q + 1], ow[4 * q + 2], ow[4 * q + 3]);
+          ptx::st_row16<D>((uint16_t*)(isk ? p.dk : p.dv) +
+                               ((SW ? (size_t)j * p.B + b : (size_t)b * p.L + j) * p.H + u.h) * X.dreal,
+                           ow, X.dreal);
         }
       }
     }

@@ -667,10 +667,7 @@ __global__ void __launch_bounds__(FwdCfg<D>::kThreads, 1)
                 ow[d / 2] = F16 ? ptx::pack_f16(o0, o1) : ptx::pack_bf16(o0, o1);
               }
             }
-            uint4* dst = (uint4*)((uint16_t*)p.o + orow);
-#pragma unroll
-            for (int v = 0; v < D / 8; ++v)
-              if (v * 8 < dreal) dst[v] = make_uint4(ow[4 * v], ow[4 * v + 1], ow[4 * v + 2], ow[4 * v + 3]);
+            ptx::st_row16<D>((uint16_t*)p.o + orow, ow, dreal);
           } else {
             uint32_t ow[D / 2];
 #pragma unroll
@@ -678,10 +675,8 @@ __global__ void __launch_bounds__(FwdCfg<D>::kThreads, 1)
               const float o0 = __uint_as_float(ov[d]) * inv, o1 = __uint_as_float(ov[d + 1]) * inv;
               ow[d / 2] = F16 ? ptx::pack_f16(o0, o1) : ptx::pack_bf16(o0, o1);
             }
-            uint4* dst = (uint4*)((uint16_t*)p.o +
-                                   ((p.swapped ? (size_t)i * p.B + b : (size_t)b * p.L + i) * p.H + si.h) * D);
-#pragma unroll
-            for (int v = 0; v < D / 8; ++v) dst[v] = make_uint4(ow[4 * v], ow[4 * v + 1], ow[4 * v + 2], ow[4 * v + 3]);
+            ptx::st_row16<D>((uint16_t*)p.o + ((p.swapped ? (size_t)i * p.B + b : (size_t)b * p.L + i) * p.H + si.h) * D,
+                             ow, D);
           }
           const float lv = l_run > 0.f ? (m_run + __log2f(l_run)) * kLn2 : -INFINITY;
           p.lse[((size_t)b * p.H + si.h) * p.L + i] = lv;

@@ -146,6 +146,25 @@ __device__ __forceinline__ void tma_store_4d(const CUtensorMap* m, const void* s
       "r"(smem_u32(src)), "r"(c0), "r"(c1), "r"(c2), "r"(c3)
       : "memory");
 }
+// One output row of D 16-bit values (packed pairs in w) to global memory: 256-bit stores (whole 32-byte
+// sectors per request, sm_100) when the row is 32-byte aligned, else 16-byte stores. `dreal` < D: only
+// the first dreal values are written (zero-padded head dim).
+template <int D>
+__device__ __forceinline__ void st_row16(void* dst, const uint32_t* w, int dreal) {
+  if (D % 16 == 0 && dreal == D && ((uintptr_t)dst & 31u) == 0) {
+#pragma unroll
+    for (int q = 0; q < D / 16; ++q)
+      asm volatile("st.global.v8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"((char*)dst + 32 * q), "r"(w[8 * q]),
+                   "r"(w[8 * q + 1]), "r"(w[8 * q + 2]), "r"(w[8 * q + 3]), "r"(w[8 * q + 4]), "r"(w[8 * q + 5]),
+                   "r"(w[8 * q + 6]), "r"(w[8 * q + 7])
+                   : "memory");
+  } else {
+#pragma unroll
+    for (int q = 0; q < D / 8; ++q)
+      if (q * 8 < dreal) ((uint4*)dst)[q] = make_uint4(w[4 * q], w[4 * q + 1], w[4 * q + 2], w[4 * q + 3]);
+  }
+}
+
 __device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
 template <int N>
 __device__ __forceinline__ void bulk_wait_read() {
