@@ -26,6 +26,7 @@ KEYS = [
     ("sm__inst_executed_pipe_xu.avg.pct_of_peak_sustained_active", "XU (MUFU) pipe %"),
     ("l1tex__data_pipe_lsu_wavefronts_mem_shared.sum", "LSU shared wavefronts"),
     ("l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum", "shared bank conflicts"),
+    ("l1tex__data_pipe_tc_wavefronts_mem_shared.sum", "tensor-core shared wavefronts"),
     ("lts__t_bytes.sum", "L2 bytes"),
     ("sm__warps_active.avg.pct_of_peak_sustained_active", "achieved occupancy %"),
     ("launch__registers_per_thread", "registers/thread"),
@@ -61,7 +62,7 @@ def full(rep, out, config, traffic_path):
     rows = list(csv.reader(io.StringIO(raw)))
     h = rows[0]
     recs = [dict(zip(h, r)) for r in rows[2:] if len(r) == len(h)]
-    traffic = {}
+    traffic, call = {}, {}
     if traffic_path and os.path.exists(traffic_path):
         traffic = json.load(open(traffic_path))
     with open(out, "w") as f:
@@ -87,8 +88,12 @@ def full(rep, out, config, traffic_path):
                 key = f"{config}_{'bwd' if 'bwd' in name else 'fwd'}_tcgen05"
                 if "bwd_kernel" in name or "fwd_kernel" in name:
                     traffic[key] = (rd + wr) * mult
+                if any(k in name for k in ("prep_kernel", "bwd_kernel", "dq_convert")):
+                    call[name] = (rd + wr) * mult  # the backward call: preamble + main kernel + conversion
             except (KeyError, ValueError):
                 pass
+    if len(call) == 3:
+        traffic[f"{config}_bwd_call_tcgen05"] = sum(call.values())
     if traffic_path:
         json.dump(traffic, open(traffic_path, "w"), indent=1, sort_keys=True)
     print(open(out).read())
