@@ -40,17 +40,62 @@ class ShardedStep:
     dv: torch.Tensor
     dbias1: Optional[torch.Tensor]
     dbias2: Optional[torch.Tensor]
-    pending: Optional[object] = None  # in-flight dBias2 all-reduce (async_reduce)
-    dbias_dtype: torch.dtype = torch.float32
+    pending: Optional[object] = None  # in-flight dBias2 reduction (async_reduce)
 
     def wait(self) -> "ShardedStep":
-        """Make the current stream wait for the in-flight dBias2 all-reduce; dbias2 is then final."""
+        """Make the current stream wait for the in-flight dBias2 reduction; dbias2 is then final."""
         if self.pending is not None:
             self.pending.wait()
             self.pending = None
-            if self.dbias2 is not None and self.dbias_dtype != torch.float32:
-                self.dbias2 = self.dbias2.to(self.dbias_dtype)
         return self
+
+
+_SIDE = {}
+
+
+def _side_stream(device):
+    if device not in _SIDE:
+        _SIDE[device] = torch.cuda.Stream(device)
+    return _SIDE[device]
+
+
+def reduce_dbias2(db2, dbias_dtype=torch.float32, group=None, async_op=False):
+    """Sum the ranks' fp32 dBias2 partials; returns (result, pending work or None).
+
+    fp32 result: one fp32 all-reduce. 16-bit result (§8(f)3, the dBias convert fused into the
+    all-reduce): reduce-scatter of the fp32 partials, each rank converts its 1/world shard, all-gather
+    of the 16-bit shards — no full-size conversion pass, and the gather half moves 16-bit values (3/4
+    of the fp32 all-reduce's bytes). The sum is fp32 either way (the reference's UpcastF32 policy,
+    attention_tiled.cpp:318-323); only the final value is rounded. async_op: the collectives (and the
+    shard conversion, on a side stream) are ordered after the work queued so far and overlap what the
+    caller queues next; wait() on the returned work before reading the result.
+    """
+    if dbias_dtype == torch.float32:
+        return db2, dist.all_reduce(db2, op=dist.ReduceOp.SUM, group=group, async_op=async_op)
+    world = dist.get_world_size(group)
+    n = db2.numel()
+    per = -(-n // world)
+    flat = db2.reshape(-1)
+    if per * world != n:
+        flat = torch.cat([flat, flat.new_zeros(per * world - n)])
+    shard = flat.new_empty(per)
+    out = torch.empty(per * world, dtype=dbias_dtype, device=db2.device)
+    res = out[:n].view(db2.shape)
+    if async_op and db2.is_cuda:
+        rs = dist.reduce_scatter_tensor(shard, flat, op=dist.ReduceOp.SUM, group=group, async_op=True)
+        side = _side_stream(db2.device)
+        with torch.cuda.stream(side):
+            rs.wait()  # the side stream waits for the reduce-scatter (not the compute stream)
+            s16 = shard.to(dbias_dtype)
+            ag = dist.all_gather_into_tensor(out, s16, group=group, async_op=True)
+        for t in (flat, shard, s16, out):
+            t.record_stream(side)
+        return res, ag
+    work = dist.reduce_scatter_tensor(shard, flat, op=dist.ReduceOp.SUM, group=group, async_op=async_op)
+    if work is not None:
+        work.wait()
+    work = dist.all_gather_into_tensor(out, shard.to(dbias_dtype), group=group, async_op=async_op)
+    return res, work
 
 
 def sharded_fwd_bwd(q, k, v, dout, bias1, bias2, group=None, dbias_dtype: torch.dtype = torch.float32,
@@ -60,7 +105,8 @@ def sharded_fwd_bwd(q, k, v, dout, bias1, bias2, group=None, dbias_dtype: torch.
 
     q/k/v/dout/bias1 are this rank's rows ([Bo, n_local, L, H, D]); bias2 is the full pair bias.
     The kernels reduce this rank's rows of dS into an fp32 dBias2 partial; one fp32 sum
-    all-reduce over the group completes it. The mask-bias gradient is off by
+    all-reduce over the group completes it — or, for a 16-bit dbias_dtype, an fp32
+    reduce-scatter, the per-shard conversion and a 16-bit all-gather (`reduce_dbias2`). The mask-bias gradient is off by
     default (the MSA mask carries no gradient in OpenFold; the headline step produces dQ, dK, dV
     and dBias2). `ops` = (forward, backward) overrides the CUDA operators (used by the CPU
     gloo tests to drive the same control flow with the oracle). async_reduce: the all-reduce is
@@ -97,12 +143,10 @@ def sharded_fwd_bwd(q, k, v, dout, bias1, bias2, group=None, dbias_dtype: torch.
             dout, q, k, v, o, lse, bias1, bias2, need_dbias1=need1,
             need_dbias2=bias2 is not None, dbias_dtype=torch.float32, **kw)
         if db2 is not None and world > 1:
-            if async_reduce:
-                work = dist.all_reduce(db2, op=dist.ReduceOp.SUM, group=group, async_op=True)
-                if db1 is not None and dbias_dtype != torch.float32:
-                    db1 = db1.to(dbias_dtype)
-                return ShardedStep(o, lse, dq, dk, dv, db1, db2, pending=work, dbias_dtype=dbias_dtype)
-            dist.all_reduce(db2, op=dist.ReduceOp.SUM, group=group)
+            db2, work = reduce_dbias2(db2, dbias_dtype, group, async_op=async_reduce)
+            if db1 is not None and dbias_dtype != torch.float32:
+                db1 = db1.to(dbias_dtype)
+            return ShardedStep(o, lse, dq, dk, dv, db1, db2, pending=work if async_reduce else None)
     if db2 is not None and dbias_dtype != torch.float32:
         db2 = db2.to(dbias_dtype)
     if db1 is not None and dbias_dtype != torch.float32:

@@ -100,3 +100,38 @@ def test_gloo_two_ranks_match_full_problem(tmp_path):
         assert np.abs(np.load(tmp_path / f"red{rank}.npy") - db2).max() / scale < 1e-6
     r0, r1 = np.load(tmp_path / "rank0.npz"), np.load(tmp_path / "rank1.npz")
     np.testing.assert_array_equal(r0["db2"], r1["db2"])  # every rank holds the same reduced gradient
+
+
+def _worker_bf16(rank, world, port, out_dir, async_op):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        Bo, Nr, L, H, D = SHAPE
+        q, k, v, do, b1, b2 = (None if a is None else torch.from_numpy(a)
+                               for a in make_inputs(*SHAPE, dtype="f32", seed=11))
+        lo, hi = shard_rows(Nr, world, rank)
+        sl = lambda t: t[:, lo:hi].contiguous()
+        step = sharded_fwd_bwd(sl(q), sl(k), sl(v), sl(do), sl(b1), b2, ops=_oracle_ops(),
+                               dbias_dtype=torch.bfloat16, async_reduce=async_op).wait()
+        assert step.dbias2.dtype == torch.bfloat16 and step.dbias2.shape == b2.shape
+        np.save(os.path.join(out_dir, f"db2_{rank}.npy"), step.dbias2.float().numpy())
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,async_op", [(2, False), (3, True)])
+def test_gloo_bf16_dbias_fused_into_the_reduction(tmp_path, world, async_op):
+    """16-bit dBias2 (§8(f)3): fp32 reduce-scatter, per-shard conversion, 16-bit all-gather. Every
+    rank holds the same bf16 gradient, equal to the fp32 full-problem sum rounded once (up to one
+    bf16 ulp where the fp32 summation order moves a value across a rounding boundary); world 3
+    exercises the padded last shard (H*L*L = 3200 is not a multiple of 3)."""
+    mp.start_processes(_worker_bf16, args=(world, _free_port(), str(tmp_path), async_op), nprocs=world,
+                       join=True, start_method="spawn")
+    q, k, v, do, b1, b2 = make_inputs(*SHAPE, dtype="f32", seed=11)
+    db2 = oracle_fwd_bwd(q, k, v, do, b1, b2)[6]
+    want = torch.from_numpy(np.ascontiguousarray(db2)).to(torch.float32).to(torch.bfloat16).float().numpy()
+    got = [np.load(tmp_path / f"db2_{r}.npy") for r in range(world)]
+    for g in got[1:]:
+        np.testing.assert_array_equal(g, got[0])
+    ulp = np.abs(want) * 2.0 ** -7 + 1e-30
+    assert np.all(np.abs(got[0] - want) <= ulp)

@@ -2,7 +2,8 @@
   1. strong sharding of one problem (rows split over ranks): every rank's O / dQ / dK / dV rows are
      bit-identical to the single-GPU run of the whole problem, and the all-reduced dBias2 equals the
      single-GPU dBias2 up to fp32 summation order (blocking and asynchronous all-reduce);
-  2. the in-kernel NVLS dBias2 reduction (EVO_MULTICAST=1, multimem.red through an NVSwitch multicast
+  2. the 16-bit dBias2 path (conversion fused into the reduction) against the fp32 sum;
+  3. the in-kernel NVLS dBias2 reduction (EVO_MULTICAST=1, multimem.red through an NVSwitch multicast
      mapping) against the NCCL all-reduce, where symmetric memory with multicast is available.
 
   python -m torch.distributed.run --nproc-per-node 2 --master-addr 127.0.0.1 tools/mgpu_check.py
@@ -46,6 +47,18 @@ for mode in ("blocking", "async"):
     print(f"rank {rank} [{mode} NCCL]: rows {lo}..{hi - 1} bit-identical to the 1-GPU run: {rows_equal}; "
           f"dBias2 max rel diff vs 1 GPU {err:.2e}", flush=True)
     ok &= rows_equal and err < 1e-5
+
+# 16-bit dBias2 with the conversion fused into the reduction (fp32 reduce-scatter, per-shard convert,
+# bf16 all-gather): equal to the fp32 sum rounded once, up to one bf16 ulp
+for mode in ("blocking", "async"):
+    r = sharded.sharded_fwd_bwd(*mine, async_reduce=(mode == "async"), dbias_dtype=torch.bfloat16).wait()
+    torch.cuda.synchronize()
+    want = ref.dbias2.to(torch.bfloat16).float()
+    ok16 = r.dbias2.dtype == torch.bfloat16 and bool(
+        ((r.dbias2.float() - want).abs() <= want.abs() * 2.0 ** -7 + 1e-30).all())
+    print(f"rank {rank} [{mode} bf16 reduce-scatter/convert/all-gather]: within one bf16 ulp of the 1-GPU "
+          f"fp32 sum: {ok16}", flush=True)
+    ok &= ok16
 
 # in-kernel multicast (NVLS) reduction vs NCCL
 os.environ["EVO_MULTICAST"] = "1"
