@@ -162,6 +162,28 @@ evo_status evo_random_uniform(uint64_t seed, uint64_t stream, int64_t skip, int6
 evo_status evo_random_mask(uint64_t seed, uint64_t stream, int64_t rows, int64_t row0, int64_t L,
                            double rate, double neg, evo_dtype dtype, void* host_out);
 
+/* Pair-bias projection feeding bias2 (no reference counterpart — OpenFold's
+ * MSARowAttentionWithPairBias layer_norm_z + linear_z, SPEC.md:153 lists it as a non-goal):
+ *   bias2[b, 0, h, i, j] = sum_c LN(z[b, i, j, :])_c * w[c, h],  LN(x) = (x - mean) / sqrt(var + eps) * ln_w + ln_b
+ * z [Bo, L, L, C] (bf16 / f16), ln_w / ln_b [C] fp32, w [C, H] fp32 (nn.Linear(C, H).weight transposed);
+ * bias2 [Bo, 1, H, L, L] in z's dtype — the layout evo_attn_fwd / evo_attn_bwd read. The backward takes
+ * dbias2 in that same layout (fp32 — evo_attn_bwd's UpcastF32 output — or z's dtype) and writes dz (z's
+ * dtype) and fp32 dln_w, dln_b, dw (per-CTA partials in the caller's workspace, summed in a fixed order:
+ * deterministic). Envelope: C a multiple of 32 up to 256, H <= 16. */
+typedef struct {
+  int64_t Bo, L, C, H;
+  evo_dtype dtype;       /* z, bias2, dz */
+  evo_dtype dbias_dtype; /* the backward's dbias2 input: EVO_F32 or dtype */
+  float eps;
+} evo_pair_bias_desc;
+
+evo_status evo_pair_bias_fwd(const evo_pair_bias_desc* desc, const void* z, const float* ln_w, const float* ln_b,
+                             const float* w, void* bias2, evo_stream_t stream);
+size_t evo_pair_bias_bwd_workspace_size(const evo_pair_bias_desc* desc);
+evo_status evo_pair_bias_bwd(const evo_pair_bias_desc* desc, const void* dbias2, const void* z, const float* ln_w,
+                             const float* ln_b, const float* w, void* dz, float* dln_w, float* dln_b, float* dw,
+                             void* workspace, size_t workspace_bytes, evo_stream_t stream);
+
 /* Library version string, e.g. "evoattn 0.1 sm_100a". */
 const char* evo_attn_version(void);
 

@@ -11,6 +11,7 @@ from .evoformer_attention import (DS4Sci_EvoformerAttention, EvoformerAttentionF
                                   evoformer_attention_backward, evoformer_attention_backward_gated,
                                   evoformer_attention_forward, evoformer_attention_forward_gated,
                                   last_launch_count, numeric_checks, resolved_path, set_numeric_checks)
+from .pair_bias import PairBiasFunction, pair_bias, pair_bias_backward, pair_bias_forward
 from .variants import (AttentionVariant, chunked_forward, layout_from_msa, variant_attention, variant_forward,
                        variant_from_name)
 
@@ -21,4 +22,5 @@ __all__ = [
     "AttentionVariant", "variant_attention", "variant_from_name", "layout_from_msa",
     "chunked_forward", "variant_forward", "set_numeric_checks", "numeric_checks",
     "evoformer_attention_forward_gated", "evoformer_attention_backward_gated",
+    "pair_bias", "pair_bias_forward", "pair_bias_backward", "PairBiasFunction",
 ]

@@ -19,6 +19,7 @@ EXPORTED = (
     "evo_attn_fwd_workspace_size", "evo_attn_bwd_workspace_size", "evo_attn_fwd", "evo_attn_bwd",
     "evo_attn_resolved_path", "evo_attn_resolved_bwd_path", "evo_attn_last_launch_count", "evo_attn_last_error",
     "evo_attn_version", "evo_random_uniform", "evo_random_mask", "evo_attn_fwd_gated", "evo_attn_bwd_gated",
+    "evo_pair_bias_fwd", "evo_pair_bias_bwd_workspace_size", "evo_pair_bias_bwd",
 )
 
 
@@ -29,6 +30,11 @@ class Desc(C.Structure):
                 ("path", C.c_int), ("dbias2_multicast", C.c_void_p), ("need_dbias1", C.c_int),
                 ("axes_swapped", C.c_int), ("check_numerics", C.c_int), ("deterministic", C.c_int),
                 ("has_gate", C.c_int)]
+
+
+class PairBiasDesc(C.Structure):
+    _fields_ = [("Bo", C.c_int64), ("L", C.c_int64), ("C", C.c_int64), ("H", C.c_int64),
+                ("dtype", C.c_int), ("dbias_dtype", C.c_int), ("eps", C.c_float)]
 
 
 _lib = None
@@ -72,6 +78,14 @@ def load(build_if_missing: bool = True):
         lib.evo_attn_bwd_gated.argtypes = [dp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, C.c_int,
                                            vp, sz, vp]
         lib.evo_attn_bwd_gated.restype = C.c_int
+    if hasattr(lib, "evo_pair_bias_fwd"):
+        pd = C.POINTER(PairBiasDesc)
+        lib.evo_pair_bias_fwd.argtypes = [pd, vp, vp, vp, vp, vp, vp]
+        lib.evo_pair_bias_fwd.restype = C.c_int
+        lib.evo_pair_bias_bwd_workspace_size.argtypes = [pd]
+        lib.evo_pair_bias_bwd_workspace_size.restype = sz
+        lib.evo_pair_bias_bwd.argtypes = [pd, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, sz, vp]
+        lib.evo_pair_bias_bwd.restype = C.c_int
     if not hasattr(lib, "evo_random_uniform"):  # an older A/B variant (tools/ab_time.py)
         _lib = lib
         return lib

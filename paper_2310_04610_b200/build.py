@@ -22,7 +22,7 @@ FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-I", os.path.
          "--expt-relaxed-constexpr", "-Xptxas", "-warn-spills"] + os.environ.get("EVO_NVCC_EXTRA", "").split()
 # (source, extra flags): tc_kernels.cu compiles as three parallel translation units (forward,
 # backward D = 32, backward D = 16; see EVO_TU there)
-SOURCES = [("evoattn_capi.cu", []), ("evoattn_inputs.cu", []), ("tc_kernels.cu", ["-DEVO_TU=1"]),
+SOURCES = [("evoattn_capi.cu", []), ("evoattn_inputs.cu", []), ("pair_bias.cu", []), ("tc_kernels.cu", ["-DEVO_TU=1"]),
            ("tc_kernels.cu", ["-DEVO_TU=2"]), ("tc_kernels.cu", ["-DEVO_TU=3"])]
 
 

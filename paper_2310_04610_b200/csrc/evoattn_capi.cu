@@ -242,6 +242,10 @@ evo_status numeric_end(const evo_attn_desc* d, const int* flag, cudaStream_t st,
 
 }  // namespace
 
+namespace evo {
+void set_last_error(const char* msg) { g_err = msg; }  // errors of the other translation units
+}  // namespace evo
+
 extern "C" {
 
 const char* evo_attn_version(void) { return "evoattn 0.2 sm_100a"; }

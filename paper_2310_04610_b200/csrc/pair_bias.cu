@@ -1,0 +1,490 @@
+// pair_bias.cu — the pair-bias projection that feeds the attention's bias2:
+//
+//   bias2[b, h, i, j] = sum_c LN(z[b, i, j, :])_c * W[c, h],   LN(x) = (x - mean) * rstd * gamma + beta
+//
+// (OpenFold's MSARowAttentionWithPairBias: layer_norm_z then linear_z without bias; the reference has
+// no counterpart, SPEC.md:153 lists projections as non-goals). The forward writes straight into the
+// [Bo, 1, H, L, L] layout K1 / K3 read (no permute / contiguous pass over the bias); the backward
+// consumes K3's dBias2 in that same layout (fp32, or the 16-bit type) — no transpose, no rounding of
+// dBias2 on the way. Both passes are HBM-bound over z (c_z channels per (i, j)): one warp per (i, j)
+// row, c_z / 32 channels per lane, LayerNorm statistics by warp shuffles; a CTA owns 32 consecutive j
+// of one (b, i) so the per-head bias rows it writes (or dBias2 rows it reads) are contiguous.
+// The weight gradients are per-CTA partial sums reduced in a fixed order (deterministic).
+#include <cuda_bf16.h>
+#include <cuda_fp16.h>
+
+#include <algorithm>
+#include <cmath>
+#include <string>
+
+#include "common.cuh"
+#include "evoattn.h"
+
+namespace evo {
+void set_last_error(const char* msg);  // evoattn_capi.cu
+}
+
+namespace {
+
+constexpr int kWarps = 8, kRowsPerWarp = 4, kTileJ = kWarps * kRowsPerWarp;  // 32 j per CTA
+
+__device__ __forceinline__ float warp_sum(float v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// CPL consecutive 16-bit values of one lane (2 * CPL bytes, naturally aligned): one vector access
+template <int CPL> struct Vec { using type = unsigned short; };
+template <> struct Vec<2> { using type = uint32_t; };
+template <> struct Vec<4> { using type = uint2; };
+template <> struct Vec<8> { using type = uint4; };
+
+template <typename T, int CPL>
+__device__ __forceinline__ void load_row(const T* p, float* x) {
+  union { typename Vec<CPL>::type v; T e[CPL]; } u;
+  u.v = *(const typename Vec<CPL>::type*)p;
+#pragma unroll
+  for (int k = 0; k < CPL; ++k) x[k] = evo::to_f(u.e[k]);
+}
+
+template <typename T, int CPL>
+__device__ __forceinline__ void store_row(T* p, const float* x) {
+  union { typename Vec<CPL>::type v; T e[CPL]; } u;
+#pragma unroll
+  for (int k = 0; k < CPL; ++k) u.e[k] = evo::from_f<T>(x[k]);
+  *(typename Vec<CPL>::type*)p = u.v;
+}
+
+// LayerNorm statistics of one row held CPL channels per lane (two-pass, fp32)
+template <int CPL>
+__device__ __forceinline__ void ln_stats(const float* x, int C, float eps, float& mean, float& rstd) {
+  float s = 0.f;
+#pragma unroll
+  for (int k = 0; k < CPL; ++k) s += x[k];
+  mean = warp_sum(s) / (float)C;
+  float v = 0.f;
+#pragma unroll
+  for (int k = 0; k < CPL; ++k) v += (x[k] - mean) * (x[k] - mean);
+  rstd = rsqrtf(warp_sum(v) / (float)C + eps);
+}
+
+// Sum of v[0..HM) over the warp, scattered: afterwards lane l holds the total of head
+// h = scatter_head<HM>(l) (halving exchanges, then plain butterflies: HM - 1 + 5 - log2 HM shuffles
+// instead of 5 HM)
+template <int HM>
+__device__ __forceinline__ float warp_sum_scatter(float* v, int lane) {
+  int n = HM;
+#pragma unroll
+  for (int off = 16; off >= 1; off >>= 1) {
+    if (n > 1) {
+      const bool up = lane & off;
+#pragma unroll
+      for (int k = 0; k < HM / 2; ++k)
+        if (k < n / 2) {
+          const float mine = up ? v[k + n / 2] : v[k], other = up ? v[k] : v[k + n / 2];
+          v[k] = mine + __shfl_xor_sync(0xffffffffu, other, off);
+        }
+      n >>= 1;
+    } else {
+      v[0] += __shfl_xor_sync(0xffffffffu, v[0], off);
+    }
+  }
+  return v[0];
+}
+template <int HM>
+__device__ __forceinline__ int scatter_head(int lane) {  // the head warp_sum_scatter leaves in `lane`
+  int h = 0, n = HM;
+#pragma unroll
+  for (int off = 16; off >= 1 && n > 1; off >>= 1, n >>= 1)
+    if (lane & off) h += n / 2;
+  return h;
+}
+
+// W [C][H] fp32 into shared memory as ws[(k * HM + h) * 32 + lane] = W[lane * CPL + k][h] (0 past H):
+// lane-contiguous, conflict-free reads
+template <int CPL, int HM>
+__device__ __forceinline__ void stage_w(const float* __restrict__ w, float* ws, int H) {
+  for (int t = threadIdx.x; t < CPL * HM * 32; t += blockDim.x) {
+    const int ln = t % 32, h = (t / 32) % HM, k = t / (32 * HM);
+    ws[t] = h < H ? w[(size_t)(ln * CPL + k) * H + h] : 0.f;
+  }
+}
+
+template <typename T, int CPL, int HM>
+__global__ void __launch_bounds__(kWarps * 32) pair_bias_fwd_kernel(const T* __restrict__ z, const float* __restrict__ gam,
+                                                                    const float* __restrict__ bet,
+                                                                    const float* __restrict__ w, T* __restrict__ out,
+                                                                    int Bo, int L, int C, int H, float eps) {
+  __shared__ float tile[HM][kTileJ];
+  extern __shared__ float ws[];  // CPL * HM * 32
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const int nj = (L + kTileJ - 1) / kTileJ;
+  const long long ntiles = (long long)Bo * L * nj;
+  const int c0 = lane * CPL;
+  stage_w<CPL, HM>(w, ws, H);
+  float g[CPL], be[CPL];
+#pragma unroll
+  for (int k = 0; k < CPL; ++k) {
+    g[k] = gam[c0 + k];
+    be[k] = bet[c0 + k];
+  }
+  const int hl = scatter_head<HM>(lane);
+  for (long long tix = blockIdx.x; tix < ntiles; tix += gridDim.x) {
+    const int jt = (int)(tix % nj), i = (int)((tix / nj) % L), b = (int)(tix / ((long long)nj * L));
+    // the warp's rows: all loads in flight together (clamped: rows past L are not stored), the
+    // reductions of the rows interleaved (a next-tile prefetch raised registers and measured slower)
+    float x[kRowsPerWarp][CPL];
+#pragma unroll
+    for (int r = 0; r < kRowsPerWarp; ++r) {
+      const int j = min(jt * kTileJ + warp * kRowsPerWarp + r, L - 1);
+      load_row<T, CPL>(z + (((size_t)b * L + i) * L + j) * C + c0, x[r]);
+    }
+    float mean[kRowsPerWarp], rstd[kRowsPerWarp];
+#pragma unroll
+    for (int r = 0; r < kRowsPerWarp; ++r) {
+      float sm = 0.f;
+#pragma unroll
+      for (int k = 0; k < CPL; ++k) sm += x[r][k];
+      mean[r] = sm;
+    }
+#pragma unroll
+    for (int r = 0; r < kRowsPerWarp; ++r) mean[r] = warp_sum(mean[r]) / (float)C;
+#pragma unroll
+    for (int r = 0; r < kRowsPerWarp; ++r) {
+      float v = 0.f;
+#pragma unroll
+      for (int k = 0; k < CPL; ++k) v += (x[r][k] - mean[r]) * (x[r][k] - mean[r]);
+      rstd[r] = v;
+    }
+#pragma unroll
+    for (int r = 0; r < kRowsPerWarp; ++r) rstd[r] = rsqrtf(warp_sum(rstd[r]) / (float)C + eps);
+#pragma unroll
+    for (int r = 0; r < kRowsPerWarp; ++r)
+#pragma unroll
+      for (int k = 0; k < CPL; ++k) x[r][k] = (x[r][k] - mean[r]) * rstd[r] * g[k] + be[k];  // y
+    __syncthreads();  // W staged (first tile); the previous tile's results written out
+    float acc[kRowsPerWarp][HM];
+#pragma unroll
+    for (int r = 0; r < kRowsPerWarp; ++r)
+#pragma unroll
+      for (int h = 0; h < HM; ++h) acc[r][h] = 0.f;
+#pragma unroll
+    for (int k = 0; k < CPL; ++k)
+#pragma unroll
+      for (int h = 0; h < HM; ++h) {
+        const float wv = ws[(k * HM + h) * 32 + lane];
+#pragma unroll
+        for (int r = 0; r < kRowsPerWarp; ++r) acc[r][h] = fmaf(x[r][k], wv, acc[r][h]);
+      }
+#pragma unroll
+    for (int r = 0; r < kRowsPerWarp; ++r) {
+      const float t = warp_sum_scatter<HM>(acc[r], lane);
+      if ((lane & (32 / HM - 1)) == 0) tile[hl][warp * kRowsPerWarp + r] = t;
+    }
+    __syncthreads();
+    for (int t = threadIdx.x; t < H * kTileJ; t += blockDim.x) {
+      const int h = t / kTileJ, jj = t % kTileJ, j = jt * kTileJ + jj;
+      if (j < L) out[(((size_t)b * H + h) * L + i) * L + j] = evo::from_f<T>(tile[h][jj]);
+    }
+  }
+}
+
+// Per CTA (grid-stride over the (b, i, j-tile) tiles): dz rows, and this CTA's partial sums of
+// dW[c][h] = sum y_c g_h, dgamma_c = sum dy_c xhat_c, dbeta_c = sum dy_c into part[blockIdx.x].
+template <typename T, typename G, int CPL, int HM>
+__global__ void __launch_bounds__(kWarps * 32, 2) pair_bias_bwd_kernel(const G* __restrict__ dbias, const T* __restrict__ z,
+                                                                    const float* __restrict__ gam,
+                                                                    const float* __restrict__ bet,
+                                                                    const float* __restrict__ w, T* __restrict__ dz,
+                                                                    float* __restrict__ part, int Bo, int L, int C,
+                                                                    int H, float eps) {
+  __shared__ float gt[HM][kTileJ];
+  extern __shared__ float dyn[];
+  float* ws = dyn;                      // CPL * HM * 32: W, lane-contiguous
+  float* red = dyn + CPL * HM * 32;     // C * H + 2 * C: the CTA's partial sums, warps added in order
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const int c0 = lane * CPL;
+  const int nj = (L + kTileJ - 1) / kTileJ;
+  const long long ntiles = (long long)Bo * L * nj;
+  stage_w<CPL, HM>(w, ws, H);
+  float g[CPL], be[CPL], dw[CPL][HM], dg[CPL], db[CPL];
+#pragma unroll
+  for (int k = 0; k < CPL; ++k) {
+    g[k] = gam[c0 + k];
+    be[k] = bet[c0 + k];
+    dg[k] = db[k] = 0.f;
+#pragma unroll
+    for (int h = 0; h < HM; ++h) dw[k][h] = 0.f;
+  }
+  // the warp's rows of z: the next tile's loaded while this one is processed
+  auto load_tile = [&](long long tx, float (*xr)[CPL]) {
+    const int jt = (int)(tx % nj), i = (int)((tx / nj) % L), b = (int)(tx / ((long long)nj * L));
+#pragma unroll
+    for (int r = 0; r < kRowsPerWarp; ++r) {
+      const int j = min(jt * kTileJ + warp * kRowsPerWarp + r, L - 1);
+      load_row<T, CPL>(z + (((size_t)b * L + i) * L + j) * C + c0, xr[r]);
+    }
+  };
+  float xn[kRowsPerWarp][CPL];
+  if (blockIdx.x < ntiles) load_tile(blockIdx.x, xn);
+  for (long long tix = blockIdx.x; tix < ntiles; tix += gridDim.x) {
+    const int jt = (int)(tix % nj), i = (int)((tix / nj) % L), b = (int)(tix / ((long long)nj * L));
+    float x[kRowsPerWarp][CPL];
+#pragma unroll
+    for (int r = 0; r < kRowsPerWarp; ++r)
+#pragma unroll
+      for (int k = 0; k < CPL; ++k) x[r][k] = xn[r][k];
+    if (tix + gridDim.x < ntiles) load_tile(tix + gridDim.x, xn);
+    __syncthreads();  // the previous tile's gradient rows were read (and W staged)
+    for (int t = threadIdx.x; t < H * kTileJ; t += blockDim.x) {
+      const int h = t / kTileJ, jj = t % kTileJ, j = jt * kTileJ + jj;
+      gt[h][jj] = j < L ? evo::to_f(dbias[(((size_t)b * H + h) * L + i) * L + j]) : 0.f;
+    }
+    float mean[kRowsPerWarp], rstd[kRowsPerWarp], dxs[kRowsPerWarp][CPL];
+#pragma unroll
+    for (int r = 0; r < kRowsPerWarp; ++r) {
+      float sm = 0.f;
+#pragma unroll
+      for (int k = 0; k < CPL; ++k) sm += x[r][k];
+      mean[r] = sm;
+    }
+#pragma unroll
+    for (int r = 0; r < kRowsPerWarp; ++r) mean[r] = warp_sum(mean[r]) / (float)C;
+#pragma unroll
+    for (int r = 0; r < kRowsPerWarp; ++r) {
+      float v = 0.f;
+#pragma unroll
+      for (int k = 0; k < CPL; ++k) v += (x[r][k] - mean[r]) * (x[r][k] - mean[r]);
+      rstd[r] = v;
+    }
+#pragma unroll
+    for (int r = 0; r < kRowsPerWarp; ++r) rstd[r] = rsqrtf(warp_sum(rstd[r]) / (float)C + eps);
+    __syncthreads();  // dBias2 rows staged
+    float gh[kRowsPerWarp][HM], s1[kRowsPerWarp], s2[kRowsPerWarp];
+#pragma unroll
+    for (int r = 0; r < kRowsPerWarp; ++r) {
+      const int jj = warp * kRowsPerWarp + r;
+      const bool valid = jt * kTileJ + jj < L;  // rows past L (clamped loads) contribute nothing
+#pragma unroll
+      for (int h = 0; h < HM; ++h) gh[r][h] = h < H && valid ? gt[h][jj] : 0.f;
+#pragma unroll
+      for (int k = 0; k < CPL; ++k) x[r][k] = (x[r][k] - mean[r]) * rstd[r];  // xhat
+      s1[r] = s2[r] = 0.f;
+    }
+#pragma unroll
+    for (int k = 0; k < CPL; ++k) {
+      float dy[kRowsPerWarp];
+#pragma unroll
+      for (int r = 0; r < kRowsPerWarp; ++r) dy[r] = 0.f;
+#pragma unroll
+      for (int h = 0; h < HM; ++h) {
+        const float wv = ws[(k * HM + h) * 32 + lane];
+        float dwa = dw[k][h];
+#pragma unroll
+        for (int r = 0; r < kRowsPerWarp; ++r) {
+          dy[r] = fmaf(wv, gh[r][h], dy[r]);
+          dwa = fmaf(x[r][k] * g[k] + be[k], gh[r][h], dwa);
+        }
+        dw[k][h] = dwa;
+      }
+#pragma unroll
+      for (int r = 0; r < kRowsPerWarp; ++r) {
+        const float xh = x[r][k];
+        dg[k] = fmaf(dy[r], xh, dg[k]);
+        db[k] += dy[r];
+        const float dxh = dy[r] * g[k];
+        s1[r] += dxh;
+        s2[r] += dxh * xh;
+        dy[r] = dxh;
+      }
+#pragma unroll
+      for (int r = 0; r < kRowsPerWarp; ++r) dxs[r][k] = dy[r];
+    }
+#pragma unroll
+    for (int r = 0; r < kRowsPerWarp; ++r) {
+      s1[r] = warp_sum(s1[r]) / (float)C;
+      s2[r] = warp_sum(s2[r]) / (float)C;
+    }
+#pragma unroll
+    for (int r = 0; r < kRowsPerWarp; ++r) {
+      const int j = jt * kTileJ + warp * kRowsPerWarp + r;
+      if (j < L) {
+        // dz = rstd * (dxhat - mean(dxhat) - xhat * mean(dxhat * xhat))
+        float dzr[CPL];
+#pragma unroll
+        for (int k = 0; k < CPL; ++k) dzr[k] = rstd[r] * (dxs[r][k] - s1[r] - x[r][k] * s2[r]);
+        store_row<T, CPL>(dz + (((size_t)b * L + i) * L + j) * C + c0, dzr);
+      }
+    }
+  }
+  // the CTA's partial sums: warps add their values in order (deterministic), then one row of `part`
+  const int nv = C * H + 2 * C;
+  for (int t = threadIdx.x; t < nv; t += blockDim.x) red[t] = 0.f;
+  for (int wv = 0; wv < kWarps; ++wv) {
+    __syncthreads();
+    if (warp == wv) {
+#pragma unroll
+      for (int k = 0; k < CPL; ++k) {
+#pragma unroll
+        for (int h = 0; h < HM; ++h)
+          if (h < H) red[(c0 + k) * H + h] += dw[k][h];
+        red[C * H + c0 + k] += dg[k];
+        red[C * H + C + c0 + k] += db[k];
+      }
+    }
+  }
+  __syncthreads();
+  for (int t = threadIdx.x; t < nv; t += blockDim.x) part[(size_t)blockIdx.x * nv + t] = red[t];
+}
+
+// out[v] = sum over the np CTA partials in ascending order; v < C*H: dW, then dgamma, dbeta
+__global__ void pair_bias_reduce_kernel(const float* __restrict__ part, int np, int nv, int CH, int C,
+                                        float* __restrict__ dw, float* __restrict__ dg, float* __restrict__ db) {
+  for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < nv; v += gridDim.x * blockDim.x) {
+    float s = 0.f;
+    for (int k = 0; k < np; ++k) s += part[(size_t)k * nv + v];
+    if (v < CH) dw[v] = s;
+    else if (v < CH + C) dg[v - CH] = s;
+    else db[v - CH - C] = s;
+  }
+}
+
+evo_status check(const evo_pair_bias_desc* d) {
+  if (!d) {
+    evo::set_last_error("null descriptor");
+    return EVO_ERR_USAGE;
+  }
+  if (d->Bo < 1 || d->L < 1 || d->C < 1 || d->H < 1) {
+    evo::set_last_error("extents must be >= 1 (Bo, L, C, H)");
+    return EVO_ERR_VALIDATION;
+  }
+  if (d->dtype != EVO_BF16 && d->dtype != EVO_F16) {
+    evo::set_last_error("z must be bf16 or f16");
+    return EVO_ERR_VALIDATION;
+  }
+  if (d->dbias_dtype != EVO_F32 && d->dbias_dtype != d->dtype) {
+    evo::set_last_error("dbias_dtype must be EVO_F32 or equal to dtype");
+    return EVO_ERR_VALIDATION;
+  }
+  if (!(d->eps > 0.f) || !std::isfinite(d->eps)) {
+    evo::set_last_error("eps must be finite and > 0");
+    return EVO_ERR_NUMERIC;
+  }
+  if (d->C % 32 != 0 || d->C > 256 || d->H > 16) {
+    evo::set_last_error("pair-bias projection supports c_z in {32, 64, ..., 256} and H <= 16");
+    return EVO_ERR_UNSUPPORTED;
+  }
+  return EVO_OK;
+}
+
+// persistent grids: up to 8 CTAs per SM walk the (b, i, j-tile) tiles
+unsigned grid_of(const evo_pair_bias_desc* d) {
+  const long long nj = (d->L + kTileJ - 1) / kTileJ, ntiles = d->Bo * d->L * nj;
+  return (unsigned)std::min<long long>(ntiles, 148LL * 8);
+}
+unsigned bwd_grid(const evo_pair_bias_desc* d) { return grid_of(d); }
+
+template <typename T, int CPL, int HM>
+void launch_fwd(const evo_pair_bias_desc* d, const void* z, const float* g, const float* b, const float* w, void* out,
+                cudaStream_t st) {
+  pair_bias_fwd_kernel<T, CPL, HM><<<grid_of(d), kWarps * 32, (size_t)CPL * HM * 32 * 4, st>>>(
+      (const T*)z, g, b, w, (T*)out, (int)d->Bo, (int)d->L, (int)d->C, (int)d->H, d->eps);
+}
+
+template <typename T, int CPL, int HM>
+void launch_bwd(const evo_pair_bias_desc* d, const void* dbias, const void* z, const float* g, const float* b,
+                const float* w, void* dz, float* part, cudaStream_t st) {
+  const size_t shm = ((size_t)CPL * HM * 32 + (size_t)(d->C * d->H + 2 * d->C)) * 4;
+  if (d->dbias_dtype == EVO_F32)
+    pair_bias_bwd_kernel<T, float, CPL, HM><<<bwd_grid(d), kWarps * 32, shm, st>>>(
+        (const float*)dbias, (const T*)z, g, b, w, (T*)dz, part, (int)d->Bo, (int)d->L, (int)d->C, (int)d->H, d->eps);
+  else
+    pair_bias_bwd_kernel<T, T, CPL, HM><<<bwd_grid(d), kWarps * 32, shm, st>>>(
+        (const T*)dbias, (const T*)z, g, b, w, (T*)dz, part, (int)d->Bo, (int)d->L, (int)d->C, (int)d->H, d->eps);
+}
+
+// dispatch over (dtype, channels per lane, head bound)
+template <template <typename, int, int> class F, typename... A>
+void dispatch(const evo_pair_bias_desc* d, A... a) {
+  const int cpl = (int)(d->C / 32);
+  auto by_h = [&](auto t, auto c) {
+    using T = decltype(t);
+    constexpr int CPL = decltype(c)::value;
+    if (d->H <= 8) F<T, CPL, 8>::run(d, a...);
+    else F<T, CPL, 16>::run(d, a...);
+  };
+  auto by_c = [&](auto t) {
+    switch (cpl) {
+      case 1: by_h(t, std::integral_constant<int, 1>{}); break;
+      case 2: by_h(t, std::integral_constant<int, 2>{}); break;
+      case 4: by_h(t, std::integral_constant<int, 4>{}); break;
+      case 8: by_h(t, std::integral_constant<int, 8>{}); break;
+      default: break;
+    }
+  };
+  if (d->dtype == EVO_BF16) by_c(__nv_bfloat16{});
+  else by_c(__half{});
+}
+
+template <typename T, int CPL, int HM>
+struct FwdOp {
+  static void run(const evo_pair_bias_desc* d, const void* z, const float* g, const float* b, const float* w,
+                  void* out, cudaStream_t st) {
+    launch_fwd<T, CPL, HM>(d, z, g, b, w, out, st);
+  }
+};
+template <typename T, int CPL, int HM>
+struct BwdOp {
+  static void run(const evo_pair_bias_desc* d, const void* dbias, const void* z, const float* g, const float* b,
+                  const float* w, void* dz, float* part, cudaStream_t st) {
+    launch_bwd<T, CPL, HM>(d, dbias, z, g, b, w, dz, part, st);
+  }
+};
+
+evo_status cuda_status() {
+  const cudaError_t e = cudaGetLastError();
+  if (e == cudaSuccess) return EVO_OK;
+  evo::set_last_error(cudaGetErrorString(e));
+  return EVO_ERR_CUDA;
+}
+
+}  // namespace
+
+extern "C" evo_status evo_pair_bias_fwd(const evo_pair_bias_desc* d, const void* z, const float* ln_w,
+                                        const float* ln_b, const float* w, void* bias2, evo_stream_t stream) {
+  if (evo_status st = check(d)) return st;
+  if (!z || !ln_w || !ln_b || !w || !bias2) {
+    evo::set_last_error("null tensor pointer");
+    return EVO_ERR_VALIDATION;
+  }
+  dispatch<FwdOp>(d, z, ln_w, ln_b, w, bias2, (cudaStream_t)stream);
+  return cuda_status();
+}
+
+extern "C" size_t evo_pair_bias_bwd_workspace_size(const evo_pair_bias_desc* d) {
+  if (check(d) != EVO_OK) return 0;
+  return (size_t)bwd_grid(d) * (size_t)(d->C * d->H + 2 * d->C) * 4;
+}
+
+extern "C" evo_status evo_pair_bias_bwd(const evo_pair_bias_desc* d, const void* dbias2, const void* z,
+                                        const float* ln_w, const float* ln_b, const float* w, void* dz,
+                                        float* dln_w, float* dln_b, float* dw, void* workspace, size_t ws_bytes,
+                                        evo_stream_t stream) {
+  if (evo_status st = check(d)) return st;
+  if (!dbias2 || !z || !ln_w || !ln_b || !w || !dz || !dln_w || !dln_b || !dw) {
+    evo::set_last_error("null tensor pointer");
+    return EVO_ERR_VALIDATION;
+  }
+  if (!workspace || ws_bytes < evo_pair_bias_bwd_workspace_size(d)) {
+    evo::set_last_error("workspace smaller than evo_pair_bias_bwd_workspace_size");
+    return EVO_ERR_VALIDATION;
+  }
+  cudaStream_t st = (cudaStream_t)stream;
+  float* part = (float*)workspace;
+  dispatch<BwdOp>(d, dbias2, z, ln_w, ln_b, w, dz, part, st);
+  const int nv = (int)(d->C * d->H + 2 * d->C);
+  pair_bias_reduce_kernel<<<(nv + 255) / 256, 256, 0, st>>>(part, (int)bwd_grid(d), nv, (int)(d->C * d->H),
+                                                              (int)d->C, dw, dln_w, dln_b);
+  return cuda_status();
+}
