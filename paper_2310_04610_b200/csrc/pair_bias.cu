@@ -19,6 +19,7 @@
 
 #include "common.cuh"
 #include "evoattn.h"
+#include "tc_ptx.cuh"
 
 namespace evo {
 void set_last_error(const char* msg);  // evoattn_capi.cu
@@ -59,14 +60,15 @@ __device__ __forceinline__ void store_row(T* p, const float* x) {
 // LayerNorm statistics of one row held CPL channels per lane (two-pass, fp32)
 template <int CPL>
 __device__ __forceinline__ void ln_stats(const float* x, int C, float eps, float& mean, float& rstd) {
+  const float invC = 1.f / (float)C;
   float s = 0.f;
 #pragma unroll
   for (int k = 0; k < CPL; ++k) s += x[k];
-  mean = warp_sum(s) / (float)C;
+  mean = warp_sum(s) * invC;
   float v = 0.f;
 #pragma unroll
   for (int k = 0; k < CPL; ++k) v += (x[k] - mean) * (x[k] - mean);
-  rstd = rsqrtf(warp_sum(v) / (float)C + eps);
+  rstd = rsqrtf(warp_sum(v) * invC + eps);
 }
 
 // Sum of v[0..HM) over the warp, scattered: afterwards lane l holds the total of head
@@ -111,18 +113,49 @@ __device__ __forceinline__ void stage_w(const float* __restrict__ w, float* ws, 
   }
 }
 
-template <typename T, int CPL, int HM>
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   evo::ptx::smem_u32(dst)),
+               "l"(src), "r"(bytes), "r"(evo::ptx::smem_u32(bar))
+               : "memory");
+}
+
+// Forward, persistent (one wave): a CTA walks (b, i, 8*FR-wide j) tiles; the tile's z rows are one
+// contiguous block, bulk-copied (TMA engine, no registers) into a double-buffered shared stage while
+// the previous tile is reduced — the HBM stream never waits on the shuffles.
+template <typename T, int CPL, int HM, int FR>
 __global__ void __launch_bounds__(kWarps * 32) pair_bias_fwd_kernel(const T* __restrict__ z, const float* __restrict__ gam,
                                                                     const float* __restrict__ bet,
                                                                     const float* __restrict__ w, T* __restrict__ out,
                                                                     int Bo, int L, int C, int H, float eps) {
-  __shared__ float tile[HM][kTileJ];
-  extern __shared__ float ws[];  // CPL * HM * 32
+  constexpr int TJ = kWarps * FR;
+  __shared__ float tile[HM][TJ];
+  __shared__ alignas(8) uint64_t full[2];
+  extern __shared__ __align__(128) unsigned char dsm[];
+  float* ws = (float*)dsm;                                     // CPL * HM * 32
+  T* stage = (T*)(dsm + (size_t)CPL * HM * 32 * 4);           // [2][TJ][C]
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
-  const int nj = (L + kTileJ - 1) / kTileJ;
-  const long long ntiles = (long long)Bo * L * nj;
+  const int nj = (L + TJ - 1) / TJ;
+  const int ntiles = Bo * L * nj;
   const int c0 = lane * CPL;
+  const float invC = 1.f / (float)C;
+  auto issue = [&](int tix, int st) {  // one thread: the tile's rows j0 .. min(j0 + TJ, L) - 1
+    const int jt = tix % nj, i = (tix / nj) % L, b = tix / (nj * L), j0 = jt * TJ;
+    const uint32_t bytes = (uint32_t)(min(TJ, L - j0) * C * (int)sizeof(T));
+    evo::ptx::mbar_expect_tx(&full[st], bytes);
+    bulk_g2s(stage + (size_t)st * TJ * C, z + (((size_t)b * L + i) * L + j0) * C, bytes, &full[st]);
+  };
+  if (threadIdx.x == 0) {
+    evo::ptx::mbar_init(&full[0], 1);
+    evo::ptx::mbar_init(&full[1], 1);
+    evo::ptx::fence_barrier_init();
+  }
   stage_w<CPL, HM>(w, ws, H);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    if ((int)blockIdx.x < ntiles) issue(blockIdx.x, 0);
+    if ((int)(blockIdx.x + gridDim.x) < ntiles) issue(blockIdx.x + gridDim.x, 1);
+  }
   float g[CPL], be[CPL];
 #pragma unroll
   for (int k = 0; k < CPL; ++k) {
@@ -130,43 +163,44 @@ __global__ void __launch_bounds__(kWarps * 32) pair_bias_fwd_kernel(const T* __r
     be[k] = bet[c0 + k];
   }
   const int hl = scatter_head<HM>(lane);
-  for (long long tix = blockIdx.x; tix < ntiles; tix += gridDim.x) {
-    const int jt = (int)(tix % nj), i = (int)((tix / nj) % L), b = (int)(tix / ((long long)nj * L));
-    // the warp's rows: all loads in flight together (clamped: rows past L are not stored), the
-    // reductions of the rows interleaved (a next-tile prefetch raised registers and measured slower)
-    float x[kRowsPerWarp][CPL];
+  int n = 0;
+  for (int tix = blockIdx.x; tix < ntiles; tix += gridDim.x, ++n) {
+    const int st = n & 1;
+    const int jt = tix % nj, i = (tix / nj) % L, b = tix / (nj * L);
+    const int nval = min(TJ, L - jt * TJ);
+    evo::ptx::mbar_wait(&full[st], (n >> 1) & 1);
+    float x[FR][CPL];
 #pragma unroll
-    for (int r = 0; r < kRowsPerWarp; ++r) {
-      const int j = min(jt * kTileJ + warp * kRowsPerWarp + r, L - 1);
-      load_row<T, CPL>(z + (((size_t)b * L + i) * L + j) * C + c0, x[r]);
-    }
-    float mean[kRowsPerWarp], rstd[kRowsPerWarp];
+    for (int r = 0; r < FR; ++r)  // rows past L read the last valid row (not stored)
+      load_row<T, CPL>(stage + ((size_t)st * TJ + min(warp * FR + r, nval - 1)) * C + c0, x[r]);
+    __syncthreads();  // stage st read by every warp; the previous tile's outputs written
+    if (threadIdx.x == 0 && tix + 2 * (int)gridDim.x < ntiles) issue(tix + 2 * gridDim.x, st);
+    float mean[FR], rstd[FR];
 #pragma unroll
-    for (int r = 0; r < kRowsPerWarp; ++r) {
+    for (int r = 0; r < FR; ++r) {
       float sm = 0.f;
 #pragma unroll
       for (int k = 0; k < CPL; ++k) sm += x[r][k];
       mean[r] = sm;
     }
 #pragma unroll
-    for (int r = 0; r < kRowsPerWarp; ++r) mean[r] = warp_sum(mean[r]) / (float)C;
+    for (int r = 0; r < FR; ++r) mean[r] = warp_sum(mean[r]) * invC;
 #pragma unroll
-    for (int r = 0; r < kRowsPerWarp; ++r) {
+    for (int r = 0; r < FR; ++r) {
       float v = 0.f;
 #pragma unroll
       for (int k = 0; k < CPL; ++k) v += (x[r][k] - mean[r]) * (x[r][k] - mean[r]);
       rstd[r] = v;
     }
 #pragma unroll
-    for (int r = 0; r < kRowsPerWarp; ++r) rstd[r] = rsqrtf(warp_sum(rstd[r]) / (float)C + eps);
+    for (int r = 0; r < FR; ++r) rstd[r] = rsqrtf(warp_sum(rstd[r]) * invC + eps);
 #pragma unroll
-    for (int r = 0; r < kRowsPerWarp; ++r)
+    for (int r = 0; r < FR; ++r)
 #pragma unroll
       for (int k = 0; k < CPL; ++k) x[r][k] = (x[r][k] - mean[r]) * rstd[r] * g[k] + be[k];  // y
-    __syncthreads();  // W staged (first tile); the previous tile's results written out
-    float acc[kRowsPerWarp][HM];
+    float acc[FR][HM];
 #pragma unroll
-    for (int r = 0; r < kRowsPerWarp; ++r)
+    for (int r = 0; r < FR; ++r)
 #pragma unroll
       for (int h = 0; h < HM; ++h) acc[r][h] = 0.f;
 #pragma unroll
@@ -175,16 +209,16 @@ __global__ void __launch_bounds__(kWarps * 32) pair_bias_fwd_kernel(const T* __r
       for (int h = 0; h < HM; ++h) {
         const float wv = ws[(k * HM + h) * 32 + lane];
 #pragma unroll
-        for (int r = 0; r < kRowsPerWarp; ++r) acc[r][h] = fmaf(x[r][k], wv, acc[r][h]);
+        for (int r = 0; r < FR; ++r) acc[r][h] = fmaf(x[r][k], wv, acc[r][h]);
       }
 #pragma unroll
-    for (int r = 0; r < kRowsPerWarp; ++r) {
+    for (int r = 0; r < FR; ++r) {
       const float t = warp_sum_scatter<HM>(acc[r], lane);
-      if ((lane & (32 / HM - 1)) == 0) tile[hl][warp * kRowsPerWarp + r] = t;
+      if ((lane & (32 / HM - 1)) == 0) tile[hl][warp * FR + r] = t;
     }
     __syncthreads();
-    for (int t = threadIdx.x; t < H * kTileJ; t += blockDim.x) {
-      const int h = t / kTileJ, jj = t % kTileJ, j = jt * kTileJ + jj;
+    for (int t = threadIdx.x; t < H * TJ; t += blockDim.x) {
+      const int h = t / TJ, jj = t % TJ, j = jt * TJ + jj;
       if (j < L) out[(((size_t)b * H + h) * L + i) * L + j] = evo::from_f<T>(tile[h][jj]);
     }
   }
@@ -205,6 +239,7 @@ __global__ void __launch_bounds__(kWarps * 32, 2) pair_bias_bwd_kernel(const G* 
   float* red = dyn + CPL * HM * 32;     // C * H + 2 * C: the CTA's partial sums, warps added in order
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const int c0 = lane * CPL;
+  const float invC = 1.f / (float)C;
   const int nj = (L + kTileJ - 1) / kTileJ;
   const long long ntiles = (long long)Bo * L * nj;
   stage_w<CPL, HM>(w, ws, H);
@@ -229,7 +264,7 @@ __global__ void __launch_bounds__(kWarps * 32, 2) pair_bias_bwd_kernel(const G* 
   float xn[kRowsPerWarp][CPL];
   if (blockIdx.x < ntiles) load_tile(blockIdx.x, xn);
   for (long long tix = blockIdx.x; tix < ntiles; tix += gridDim.x) {
-    const int jt = (int)(tix % nj), i = (int)((tix / nj) % L), b = (int)(tix / ((long long)nj * L));
+    const int t32 = (int)tix, jt = t32 % nj, i = (t32 / nj) % L, b = t32 / (nj * L);
     float x[kRowsPerWarp][CPL];
 #pragma unroll
     for (int r = 0; r < kRowsPerWarp; ++r)
@@ -250,7 +285,7 @@ __global__ void __launch_bounds__(kWarps * 32, 2) pair_bias_bwd_kernel(const G* 
       mean[r] = sm;
     }
 #pragma unroll
-    for (int r = 0; r < kRowsPerWarp; ++r) mean[r] = warp_sum(mean[r]) / (float)C;
+    for (int r = 0; r < kRowsPerWarp; ++r) mean[r] = warp_sum(mean[r]) * invC;
 #pragma unroll
     for (int r = 0; r < kRowsPerWarp; ++r) {
       float v = 0.f;
@@ -259,7 +294,7 @@ __global__ void __launch_bounds__(kWarps * 32, 2) pair_bias_bwd_kernel(const G* 
       rstd[r] = v;
     }
 #pragma unroll
-    for (int r = 0; r < kRowsPerWarp; ++r) rstd[r] = rsqrtf(warp_sum(rstd[r]) / (float)C + eps);
+    for (int r = 0; r < kRowsPerWarp; ++r) rstd[r] = rsqrtf(warp_sum(rstd[r]) * invC + eps);
     __syncthreads();  // dBias2 rows staged
     float gh[kRowsPerWarp][HM], s1[kRowsPerWarp], s2[kRowsPerWarp];
 #pragma unroll
@@ -303,8 +338,8 @@ __global__ void __launch_bounds__(kWarps * 32, 2) pair_bias_bwd_kernel(const G* 
     }
 #pragma unroll
     for (int r = 0; r < kRowsPerWarp; ++r) {
-      s1[r] = warp_sum(s1[r]) / (float)C;
-      s2[r] = warp_sum(s2[r]) / (float)C;
+      s1[r] = warp_sum(s1[r]) * invC;
+      s2[r] = warp_sum(s2[r]) * invC;
     }
 #pragma unroll
     for (int r = 0; r < kRowsPerWarp; ++r) {
@@ -371,6 +406,10 @@ evo_status check(const evo_pair_bias_desc* d) {
     evo::set_last_error("eps must be finite and > 0");
     return EVO_ERR_NUMERIC;
   }
+  if (d->Bo * d->L * d->L >= (1LL << 31)) {  // 32-bit tile / row indices
+    evo::set_last_error("pair-bias projection: Bo * L * L must be < 2^31");
+    return EVO_ERR_UNSUPPORTED;
+  }
   if (d->C % 32 != 0 || d->C > 256 || d->H > 16) {
     evo::set_last_error("pair-bias projection supports c_z in {32, 64, ..., 256} and H <= 16");
     return EVO_ERR_UNSUPPORTED;
@@ -385,11 +424,26 @@ unsigned grid_of(const evo_pair_bias_desc* d) {
 }
 unsigned bwd_grid(const evo_pair_bias_desc* d) { return grid_of(d); }
 
+#ifndef EVO_PB_FR
+#define EVO_PB_FR 4  // forward rows per warp (a CTA covers 8 * EVO_PB_FR consecutive j)
+#endif
 template <typename T, int CPL, int HM>
 void launch_fwd(const evo_pair_bias_desc* d, const void* z, const float* g, const float* b, const float* w, void* out,
                 cudaStream_t st) {
-  pair_bias_fwd_kernel<T, CPL, HM><<<grid_of(d), kWarps * 32, (size_t)CPL * HM * 32 * 4, st>>>(
-      (const T*)z, g, b, w, (T*)out, (int)d->Bo, (int)d->L, (int)d->C, (int)d->H, d->eps);
+  constexpr int FR = EVO_PB_FR;
+  auto kern = pair_bias_fwd_kernel<T, CPL, HM, FR>;
+  const size_t shm = (size_t)CPL * HM * 32 * 4 + 2 * (size_t)kWarps * FR * d->C * sizeof(T);
+  static int shm_set = 0;  // dynamic + static shared memory past 48 KB needs the opt-in
+  if ((int)shm > shm_set) {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shm);
+    shm_set = (int)shm;
+  }
+  int per_sm = 1;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kWarps * 32, shm);
+  const long long nj = (d->L + kWarps * FR - 1) / (kWarps * FR), ntiles = d->Bo * d->L * nj;
+  const unsigned grid = (unsigned)std::min<long long>(ntiles, 148LL * std::max(per_sm, 1));  // one wave
+  kern<<<grid, kWarps * 32, shm, st>>>((const T*)z, g, b, w, (T*)out, (int)d->Bo, (int)d->L, (int)d->C, (int)d->H,
+                                       d->eps);
 }
 
 template <typename T, int CPL, int HM>
