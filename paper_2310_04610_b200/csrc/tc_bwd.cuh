@@ -881,7 +881,6 @@ __global__ void prep_kernel(const T* __restrict__ dout, const T* __restrict__ o,
   // gate (fused OpenFold output gate; dout, o are the gated output's gradient and value): also writes
   // dO = dout * sigmoid(G) for the main kernel and dG = dout * o * (1 - sigmoid(G)); delta = sum dout*o
   constexpr bool swapped = SW;
-  ptx::pdl_wait();  // a programmatic dependent of the predecessor (the forward): its outputs complete
   ptx::pdl_launch_dependents();
   for (long long x = blockIdx.x * (long long)blockDim.x + threadIdx.x; x < nzero4; x += (long long)gridDim.x * blockDim.x)
     zero[x] = make_float4(0.f, 0.f, 0.f, 0.f);  // fp32 gradient accumulators of the main kernel

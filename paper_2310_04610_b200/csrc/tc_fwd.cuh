@@ -237,10 +237,6 @@ __global__ void __launch_bounds__(FwdCfg<D>::kThreads, 1)
   __syncthreads();
   ptx::tc_fence_after();
   const uint32_t tmem = *tmem_slot;
-  // launched as a programmatic dependent: the prologue above overlapped the predecessor's tail; its
-  // results (this call's inputs) are read only past this point
-  ptx::pdl_wait();
-  ptx::pdl_launch_dependents();
 
   constexpr uint32_t kSw = ptx::swizzle_code(C::kRowBytes);
   constexpr bool streamed = BM == kBiasStreamed;

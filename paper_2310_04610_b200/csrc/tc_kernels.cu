@@ -218,17 +218,7 @@ evo_status launch_fwd(const evo_attn_desc* d, const Shape& s, const void* q, con
     p.aligned = 1;
     grid = units * p.split;
   }
-  cudaLaunchConfig_t cfg = {};  // programmatic dependent launch: the prologue overlaps the predecessor's tail
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  attr[0].val.programmaticStreamSerializationAllowed = getenv("EVO_NO_PDL") ? 0 : 1;
-  cfg.gridDim = dim3((unsigned)grid);
-  cfg.blockDim = dim3(FwdCfg<D>::kThreads);
-  cfg.dynamicSmemBytes = smem;
-  cfg.stream = st;
-  cfg.attrs = attr;
-  cfg.numAttrs = 1;
-  cudaLaunchKernelEx(&cfg, kern, tq, tk, tv, tb, p);
+  kern<<<(unsigned)grid, FwdCfg<D>::kThreads, smem, st>>>(tq, tk, tv, tb, p);
   ++*launches;
   return EVO_OK;
 }
@@ -430,17 +420,9 @@ evo_status launch_bwd(const evo_attn_desc* d, const Shape& s, const void* dout, 
   } else {
     auto prep = s.D == 8 ? (s.swapped ? bk::prep_kernel<8, T, true> : bk::prep_kernel<8, T, false>)
                          : (s.swapped ? bk::prep_kernel<D, T, true> : bk::prep_kernel<D, T, false>);
-    cudaLaunchConfig_t cfg = {};  // programmatic dependent of the forward (waits for it before any access)
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    attr[0].val.programmaticStreamSerializationAllowed = getenv("EVO_NO_PDL") ? 0 : 1;
-    cfg.gridDim = dim3((unsigned)std::min<long long>((prow * Lp + 255) / 256, 148 * 32));
-    cfg.blockDim = dim3(256);
-    cfg.stream = st;
-    cfg.attrs = attr;
-    cfg.numAttrs = 1;
-    cudaLaunchKernelEx(&cfg, prep, (const T*)dout, (const T*)o, lse, lse2, delta_p, (int)s.B, (int)s.L, (int)s.H, Lp,
-                       zero4, nzero4, s.flag, (const T*)s.gate, (T*)s.dog, (T*)s.dgate);
+    prep<<<(unsigned)std::min<long long>((prow * Lp + 255) / 256, 148 * 32), 256, 0, st>>>(
+        (const T*)dout, (const T*)o, lse, lse2, delta_p, s.B, s.L, s.H, Lp, zero4, nzero4, s.flag,
+        (const T*)s.gate, (T*)s.dog, (T*)s.dgate);
   }
   ++*launches;
   const bool safe = det || win || s.flag || s.D != D;
