@@ -37,6 +37,9 @@ namespace bk {
 constexpr int kBM = 128;   // queries per tile
 constexpr int kBN = 64;    // keys per tile
 // warps: 0 TMA producer, 1 gradient MMAs, 2 S/dP MMAs, 3..3+4*kSoftWG softmax warpgroups, then the epilogue WG
+#ifndef EVO_BWD_KSTAGES
+#define EVO_BWD_KSTAGES 2  // (K, V, bias1 chunk) ring depth
+#endif
 #ifndef EVO_BWD_QSTAGES
 #define EVO_BWD_QSTAGES 4  // (Q, dO, lse, delta) ring depth of the unchunked variants
 #endif
@@ -81,7 +84,7 @@ constexpr uint32_t kDb1Col = 384;
 #ifndef EVO_BWD_EXP
 #define EVO_BWD_EXP 0  // timing experiments only (wrong results), bit mask: 1 no dK/dV MMAs, 2 no dQ MMA, 4 no bias LDS,
                        // 8 no P/dS stores, 16 no exponentials, 32 no dQ staging/reduce, 64 no dBias2 strip MMAs,
-                       // 128 every row loads the Q / dO / lse / delta of row 0 (L2-resident)
+                       // 128 every row loads the Q / dO / lse / delta of row 0 (L2-resident), 256 no bias1 UMMA step
 #endif  // dBias1 column sums (M=64, 16 columns) when requested: chunks of <= 2 q-tiles
 
 template <int D, bool CH>
@@ -95,7 +98,7 @@ struct Cfg {
   // 3-deep ring win (C5: 44.8 vs 57.6 ms)
   static constexpr int kQStages = CH ? 3 : EVO_BWD_QSTAGES;
   static constexpr int kDqBufs = (EVO_BWD_EXP & 32) && !CH ? 0 : kQStages > 3 ? 1 : 2;  // fp32 dQ staging tiles
-  static constexpr int kKStages = 2;                // (K, V, bias1 chunk) ring
+  static constexpr int kKStages = EVO_BWD_KSTAGES;  // (K, V, bias1 chunk) ring
   static constexpr int kBiasTile = kBM * kBN * 2;   // 16 KB
   static constexpr int kPdsTile = kBM * kBN * 2;    // 16 KB (P or dS, bf16)
   static constexpr int kDqStage = kBM * D * 4;      // fp32 dQ staging
@@ -571,7 +574,7 @@ __global__ void __launch_bounds__(kThreads, 1)
               ptx::mma_ss(tmem + sb * 128 + 64, ptx::desc_make(doA + kk * 2, kHiK), ptx::desc_make(vA + kk * 2, kHiK),
                           idS, kk > 0);  // dP
             }
-            if (p.aug) ptx::mma_ss(tmem + sb * 128, ptx::desc_make(aA, kHiAug), ptx::desc_make(bA, kHiAug), idS, 1u);
+            if (p.aug && !(EVO_BWD_EXP & 256)) ptx::mma_ss(tmem + sb * 128, ptx::desc_make(aA, kHiAug), ptx::desc_make(bA, kHiAug), idS, 1u);
             ptx::tc_commit(&s_full[sb]);
             trace(p, kTbSIssue, step);
           }
