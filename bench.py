@@ -404,6 +404,24 @@ def main():
                          max(10, args.steps // 4))
     del gate, og, lse_g
 
+    # the pair-bias projection feeding bias2: LayerNorm(z)·W → [Bo, 1, H, L, L] and its
+    # backward from dBias2, z = [Bo, L, L, c_z = 128] (OpenFold's pair channels), timed alone
+    pair_bias = None
+    if b2 is not None and dt != "f32":
+        cz = 128
+        zp = (torch.randn(Bo, L, L, cz, device=dev) * 2).to(q.dtype)
+        lw, lb = torch.ones(cz, device=dev), torch.zeros(cz, device=dev)
+        wz = torch.randn(H, cz, device=dev) / cz ** 0.5
+        gb = torch.randn(Bo, 1, H, L, L, device=dev)
+        pf = time_call(lambda: E.pair_bias_forward(zp, lw, lb, wz), 20)
+        pb = time_call(lambda: E.pair_bias_backward(gb, zp, lw, lb, wz), 20)
+        zbytes = zp.numel() * zp.element_size()
+        pair_bias = {"c_z": cz, "fwd_ms": pf, "bwd_ms": pb,
+                     "fwd_gbs": (zbytes + gb.numel() * zp.element_size()) / pf / 1e6,
+                     "bwd_gbs": (2 * zbytes + gb.numel() * 4) / pb / 1e6,
+                     "what": "LayerNorm(z)·W -> bias2 in the attention's layout, and its backward from fp32 dBias2"}
+        del zp, gb
+
     allreduce_us = None
     if world > 1 and b2 is not None:  # the dBias2 all-reduce alone (fp32, H*L*L), blocking on the stream
         buf = torch.zeros(b2.numel(), device=dev, dtype=torch.float32)
@@ -591,6 +609,7 @@ def main():
             "dbias2_allreduce_us": allreduce_us,
             "gated": {"ms_per_step": gated_ms, "tflops": flops(B_local, L, H, D) / gated_ms / 1e9,
                       "what": "fwd+bwd with the fused sigmoid output gate (this rank's rows, no all-reduce)"},
+            "pair_bias": pair_bias,
             "peak_mem": {"extra_bytes_per_rank": int(peak_extra), "naive_logits_bytes": naive,
                          "o_l_plan_bytes": 8 * B_local * H * L + 4 * H * L * L,
                          # the reference attn-bench column (run.cpp:223-234): naive / tiled peak
