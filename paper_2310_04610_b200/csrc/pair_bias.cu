@@ -236,7 +236,7 @@ __global__ void __launch_bounds__(kWarps * 32, 2) pair_bias_bwd_kernel(const G* 
   __shared__ float gt[HM][kTileJ];
   extern __shared__ float dyn[];
   float* ws = dyn;                      // CPL * HM * 32: W, lane-contiguous
-  float* red = dyn + CPL * HM * 32;     // C * H + 2 * C: the CTA's partial sums, warps added in order
+  float* red = dyn + CPL * HM * 32;     // CPL * (HM + 2) * 32: the CTA's partial sums, warps added in order
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const int c0 = lane * CPL;
   const float invC = 1.f / (float)C;
@@ -353,35 +353,52 @@ __global__ void __launch_bounds__(kWarps * 32, 2) pair_bias_bwd_kernel(const G* 
       }
     }
   }
-  // the CTA's partial sums: warps add their values in order (deterministic), then one row of `part`
+  // the CTA's partial sums: warps add their values in order (deterministic) into a lane-contiguous
+  // (conflict-free) layout red[(k * (HM + 2) + e) * 32 + lane], e < HM: dW, HM: dgamma, HM + 1: dbeta;
+  // then one row of `part` in the (dW[c][h], dgamma[c], dbeta[c]) order
   const int nv = C * H + 2 * C;
-  for (int t = threadIdx.x; t < nv; t += blockDim.x) red[t] = 0.f;
+  for (int t = threadIdx.x; t < CPL * (HM + 2) * 32; t += blockDim.x) red[t] = 0.f;
   for (int wv = 0; wv < kWarps; ++wv) {
     __syncthreads();
     if (warp == wv) {
 #pragma unroll
       for (int k = 0; k < CPL; ++k) {
 #pragma unroll
-        for (int h = 0; h < HM; ++h)
-          if (h < H) red[(c0 + k) * H + h] += dw[k][h];
-        red[C * H + c0 + k] += dg[k];
-        red[C * H + C + c0 + k] += db[k];
+        for (int h = 0; h < HM; ++h) red[(k * (HM + 2) + h) * 32 + lane] += dw[k][h];
+        red[(k * (HM + 2) + HM) * 32 + lane] += dg[k];
+        red[(k * (HM + 2) + HM + 1) * 32 + lane] += db[k];
       }
     }
   }
   __syncthreads();
-  for (int t = threadIdx.x; t < nv; t += blockDim.x) part[(size_t)blockIdx.x * nv + t] = red[t];
+  for (int t = threadIdx.x; t < nv; t += blockDim.x) {
+    int c, e;
+    if (t < C * H) { c = t / H; e = t % H; }
+    else if (t < C * H + C) { c = t - C * H; e = HM; }
+    else { c = t - C * H - C; e = HM + 1; }
+    part[(size_t)blockIdx.x * nv + t] = red[((c % CPL) * (HM + 2) + e) * 32 + c / CPL];
+  }
 }
 
-// out[v] = sum over the np CTA partials in ascending order; v < C*H: dW, then dgamma, dbeta
+// out[v] = sum of the np CTA partials of value v (v < C*H: dW, then dgamma, dbeta) in a fixed order:
+// a CTA owns 32 values; its 8 warps sum partials k = w, w + 8, ... (coalesced rows of 32 values), then
+// warp 0 adds the 8 warp sums in order — deterministic, and every partial row is read once
 __global__ void pair_bias_reduce_kernel(const float* __restrict__ part, int np, int nv, int CH, int C,
                                         float* __restrict__ dw, float* __restrict__ dg, float* __restrict__ db) {
-  for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < nv; v += gridDim.x * blockDim.x) {
-    float s = 0.f;
-    for (int k = 0; k < np; ++k) s += part[(size_t)k * nv + v];
-    if (v < CH) dw[v] = s;
-    else if (v < CH + C) dg[v - CH] = s;
-    else db[v - CH - C] = s;
+  __shared__ float ws8[8][32];
+  const int lane = threadIdx.x % 32, wv = threadIdx.x / 32, v = blockIdx.x * 32 + lane;
+  float s = 0.f;
+  if (v < nv)
+    for (int k = wv; k < np; k += 8) s += part[(size_t)k * nv + v];
+  ws8[wv][lane] = s;
+  __syncthreads();
+  if (wv == 0 && v < nv) {
+    float t = 0.f;
+#pragma unroll
+    for (int q = 0; q < 8; ++q) t += ws8[q][lane];
+    if (v < CH) dw[v] = t;
+    else if (v < CH + C) dg[v - CH] = t;
+    else db[v - CH - C] = t;
   }
 }
 
@@ -422,7 +439,10 @@ unsigned grid_of(const evo_pair_bias_desc* d) {
   const long long nj = (d->L + kTileJ - 1) / kTileJ, ntiles = d->Bo * d->L * nj;
   return (unsigned)std::min<long long>(ntiles, 148LL * 8);
 }
-unsigned bwd_grid(const evo_pair_bias_desc* d) { return grid_of(d); }
+unsigned bwd_grid(const evo_pair_bias_desc* d) {  // one wave at the backward's 2 CTAs per SM: fewer partials
+  const long long nj = (d->L + kTileJ - 1) / kTileJ, ntiles = d->Bo * d->L * nj;
+  return (unsigned)std::min<long long>(ntiles, 148LL * 2);
+}
 
 #ifndef EVO_PB_FR
 #define EVO_PB_FR 4  // forward rows per warp (a CTA covers 8 * EVO_PB_FR consecutive j)
@@ -449,7 +469,7 @@ void launch_fwd(const evo_pair_bias_desc* d, const void* z, const float* g, cons
 template <typename T, int CPL, int HM>
 void launch_bwd(const evo_pair_bias_desc* d, const void* dbias, const void* z, const float* g, const float* b,
                 const float* w, void* dz, float* part, cudaStream_t st) {
-  const size_t shm = ((size_t)CPL * HM * 32 + (size_t)(d->C * d->H + 2 * d->C)) * 4;
+  const size_t shm = ((size_t)CPL * HM * 32 + (size_t)CPL * (HM + 2) * 32) * 4;
   if (d->dbias_dtype == EVO_F32)
     pair_bias_bwd_kernel<T, float, CPL, HM><<<bwd_grid(d), kWarps * 32, shm, st>>>(
         (const float*)dbias, (const T*)z, g, b, w, (T*)dz, part, (int)d->Bo, (int)d->L, (int)d->C, (int)d->H, d->eps);
@@ -538,7 +558,7 @@ extern "C" evo_status evo_pair_bias_bwd(const evo_pair_bias_desc* d, const void*
   float* part = (float*)workspace;
   dispatch<BwdOp>(d, dbias2, z, ln_w, ln_b, w, dz, part, st);
   const int nv = (int)(d->C * d->H + 2 * d->C);
-  pair_bias_reduce_kernel<<<(nv + 255) / 256, 256, 0, st>>>(part, (int)bwd_grid(d), nv, (int)(d->C * d->H),
-                                                              (int)d->C, dw, dln_w, dln_b);
+  pair_bias_reduce_kernel<<<(nv + 31) / 32, 256, 0, st>>>(part, (int)bwd_grid(d), nv, (int)(d->C * d->H),
+                                                            (int)d->C, dw, dln_w, dln_b);
   return cuda_status();
 }
