@@ -256,6 +256,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-parity", action="store_true")
+    ap.add_argument("--e2e-streams", type=int, default=1,
+                    help="copy streams per direction in the end-to-end run (copy engines share the PCIe link)")
     ap.add_argument("--e2e-steps", type=int, default=20,
                     help="end-to-end steps timed (pipeline fill and drain amortised over them)")
     ap.add_argument("--all-configs", action="store_true", help="also time c1..c5 and attach them")
@@ -476,44 +478,55 @@ def main():
     host_out = [torch.empty(t.shape, dtype=t.dtype, pin_memory=True) for t in (r.dq, r.dk, r.dv, r.dbias2)]
     h2d = sum(t.numel() * t.element_size() for t in host_in)
     d2h = sum(t.numel() * t.element_size() for t in host_out)
-    s_in, s_out = torch.cuda.Stream(), torch.cuda.Stream()
+    # copies spread over args.e2e_streams streams per direction (several copy engines share PCIe)
+    ns = max(1, args.e2e_streams)
+    s_ins = [torch.cuda.Stream() for _ in range(ns)]
+    s_outs = [torch.cuda.Stream() for _ in range(ns)]
+    s_in = s_ins[0]
 
     def e2e_run(nsteps):
-        ready = [torch.cuda.Event() for _ in range(2)]
+        ready = [[torch.cuda.Event() for _ in range(ns)] for _ in range(2)]
         free = [torch.cuda.Event() for _ in range(2)]
         for f in free:
             f.record(stream)
 
         def upload(slot):
-            with torch.cuda.stream(s_in):
-                s_in.wait_event(free[slot])
-                for hs, ds in zip(host_in, dev_sets[slot]):
-                    ds.copy_(hs, non_blocking=True)
-                ready[slot].record(s_in)
+            for si, sin in enumerate(s_ins):
+                with torch.cuda.stream(sin):
+                    sin.wait_event(free[slot])
+                    for k_, (hs, ds) in enumerate(zip(host_in, dev_sets[slot])):
+                        if k_ % ns == si:
+                            ds.copy_(hs, non_blocking=True)
+                    ready[slot][si].record(sin)
 
         upload(0)
         for i in range(nsteps):
             cur = i % 2
             if i + 1 < nsteps:
                 upload(1 - cur)
-            stream.wait_event(ready[cur])
+            for ev in ready[cur]:
+                stream.wait_event(ev)
             rr = sharded_fwd_bwd(*dev_sets[cur]).wait()
             free[cur].record(stream)
             done = torch.cuda.Event()
             done.record(stream)
-            with torch.cuda.stream(s_out):
-                s_out.wait_event(done)
-                for hd, t_ in zip(host_out, (rr.dq, rr.dk, rr.dv, rr.dbias2)):
-                    t_.record_stream(s_out)
-                    hd.copy_(t_, non_blocking=True)
-        stream.wait_stream(s_out)
+            for so_i, sout in enumerate(s_outs):
+                with torch.cuda.stream(sout):
+                    sout.wait_event(done)
+                    for k_, (hd, t_) in enumerate(zip(host_out, (rr.dq, rr.dk, rr.dv, rr.dbias2))):
+                        if k_ % ns == so_i:
+                            t_.record_stream(sout)
+                            hd.copy_(t_, non_blocking=True)
+        for sout in s_outs:
+            stream.wait_stream(sout)
 
     e2e_run(2)
     torch.cuda.synchronize()
     barrier()
     a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     a.record(stream)
-    s_in.wait_stream(stream)
+    for sin in s_ins:
+        sin.wait_stream(stream)
     e2e_run(args.e2e_steps)
     b.record(stream)
     torch.cuda.synchronize()
