@@ -16,6 +16,7 @@
 #include <algorithm>
 #include <cmath>
 #include <string>
+#include <type_traits>
 
 #include "common.cuh"
 #include "evoattn.h"
@@ -220,6 +221,183 @@ __global__ void __launch_bounds__(kWarps * 32) pair_bias_fwd_kernel(const T* __r
     for (int t = threadIdx.x; t < H * TJ; t += blockDim.x) {
       const int h = t / TJ, jj = t % TJ, j = jt * TJ + jj;
       if (j < L) out[(((size_t)b * H + h) * L + i) * L + j] = evo::from_f<T>(tile[h][jj]);
+    }
+  }
+}
+
+// Forward on the tensor pipe (mma.sync m16n8k16, fp32 accumulate): with W' = diag(gamma) W rounded to
+// the 16-bit type, s1[h] = sum_c W'[c][h] and s2[h] = sum_c beta_c W[c][h],
+//   bias[row][h] = rstd_row * (z_row . W'[:, h] - mean_row * s1[h]) + s2[h]
+// — the LayerNorm folded into an epilogue, the c_z x H contraction a 64-row x C x H MMA per warp tile
+// on the raw z values (exact 16-bit inputs). The rows land in a double-buffered shared stage by bulk
+// copies, one per row at a padded pitch (C * 2 + 16 bytes: conflict-free fragment loads); the per-row
+// statistics (sum, sum of squares in fp32) come from two lanes per row.
+template <typename T, int HM>
+__global__ void __launch_bounds__(128) pair_bias_fwd_mma_kernel(const T* __restrict__ z, const float* __restrict__ gam,
+                                                              const float* __restrict__ bet,
+                                                              const float* __restrict__ w, T* __restrict__ out,
+                                                              int Bo, int L, int C, int H, float eps) {
+  constexpr int TJ = 64;           // rows per tile: 4 warps x 16
+  constexpr int NT = HM / 8;       // n tiles of 8 heads
+  constexpr int KMAX = 256 / 16;   // k steps at the largest c_z
+  __shared__ float tile[HM][TJ];
+  __shared__ float s1s[HM], s2s[HM];
+  __shared__ alignas(8) uint64_t full[2];
+  extern __shared__ __align__(128) unsigned char dsm[];
+  const int pitch = C * 2 + 16;    // bytes per staged row
+  unsigned char* stage = dsm;      // [2][TJ][pitch]
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const int nj = (L + TJ - 1) / TJ;
+  const int ntiles = Bo * L * nj;
+  const int KS = C / 16;
+  const float invC = 1.f / (float)C;
+  // B fragments (W' = gamma * W in the 16-bit type), per k step and n tile: b0 = (k 2q, 2q+1; n g),
+  // b1 = (k 8 + 2q, 9 + 2q; n g) with g = lane / 4, q = lane % 4
+  uint32_t bf[KMAX][NT][2];
+  {
+    const int g = lane / 4, q = lane % 4;
+#pragma unroll
+    for (int ks = 0; ks < KMAX; ++ks)
+#pragma unroll
+      for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+        for (int hf = 0; hf < 2; ++hf) {
+          uint32_t v = 0u;
+          const int h = nt * 8 + g, k0 = ks * 16 + hf * 8 + 2 * q;
+          if (ks < KS && h < H) {
+            T e[2];
+            e[0] = evo::from_f<T>(gam[k0] * w[(size_t)k0 * H + h]);
+            e[1] = evo::from_f<T>(gam[k0 + 1] * w[(size_t)(k0 + 1) * H + h]);
+            v = *(const uint32_t*)e;
+          }
+          bf[ks][nt][hf] = v;
+        }
+  }
+  {  // s1 from the rounded W' (consistent with the MMA), s2 in fp32: channels over the threads, then a
+     // fixed-order reduction (warp shuffles, then the 4 warps in order)
+    __shared__ float red1[4][HM], red2[4][HM];
+    float v1[HM], v2[HM];
+#pragma unroll
+    for (int h = 0; h < HM; ++h) v1[h] = v2[h] = 0.f;
+    for (int c = threadIdx.x; c < C; c += blockDim.x)
+#pragma unroll
+      for (int h = 0; h < HM; ++h)
+        if (h < H) {
+          const float wv = w[(size_t)c * H + h];
+          v1[h] += evo::to_f(evo::from_f<T>(gam[c] * wv));
+          v2[h] += bet[c] * wv;
+        }
+#pragma unroll
+    for (int h = 0; h < HM; ++h) {
+      const float a = warp_sum(v1[h]), c2 = warp_sum(v2[h]);
+      if (lane == 0) { red1[warp][h] = a; red2[warp][h] = c2; }
+    }
+    __syncthreads();
+    if (threadIdx.x < HM) {
+      float a = 0.f, c2 = 0.f;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) { a += red1[q][threadIdx.x]; c2 += red2[q][threadIdx.x]; }
+      s1s[threadIdx.x] = a;
+      s2s[threadIdx.x] = c2;
+    }
+  }
+  auto issue = [&](int tix, int st) {  // warp 0: a bulk copy per row (padded pitch), rows over the lanes
+    const int jt = tix % nj, i = (tix / nj) % L, b = tix / (nj * L), j0 = jt * TJ;
+    const int nr = min(TJ, L - j0);
+    if (lane == 0) evo::ptx::mbar_expect_tx(&full[st], (uint32_t)(nr * C * 2));
+    __syncwarp();
+    const T* src = z + (((size_t)b * L + i) * L + j0) * C;
+    for (int r = lane; r < nr; r += 32)
+      bulk_g2s(stage + ((size_t)st * TJ + r) * pitch, src + (size_t)r * C, (uint32_t)(C * 2), &full[st]);
+  };
+  if (threadIdx.x == 0) {
+    evo::ptx::mbar_init(&full[0], 1);
+    evo::ptx::mbar_init(&full[1], 1);
+    evo::ptx::fence_barrier_init();
+  }
+  __syncthreads();
+  if (warp == 0) {
+    if ((int)blockIdx.x < ntiles) issue(blockIdx.x, 0);
+    if ((int)(blockIdx.x + gridDim.x) < ntiles) issue(blockIdx.x + gridDim.x, 1);
+  }
+  int n = 0;
+  for (int tix = blockIdx.x; tix < ntiles; tix += gridDim.x, ++n) {
+    const int st = n & 1;
+    const int jt = tix % nj, i = (tix / nj) % L, b = tix / (nj * L);
+    evo::ptx::mbar_wait(&full[st], (n >> 1) & 1);
+    const unsigned char* rows = stage + ((size_t)st * TJ + warp * 16) * pitch;  // this warp's 16 rows
+    // statistics: lanes 2r, 2r+1 sum the two halves of row r
+    float sx = 0.f, sxx = 0.f;
+    {
+      const int r = lane / 2, half = lane % 2;
+      const uint4* p = (const uint4*)(rows + (size_t)r * pitch + half * C);
+      for (int c8 = 0; c8 < C / 16; ++c8) {
+        const uint4 u = p[c8];
+        const T* e = (const T*)&u;
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          const float x = evo::to_f(e[k]);
+          sx += x;
+          sxx = fmaf(x, x, sxx);
+        }
+      }
+      sx += __shfl_xor_sync(0xffffffffu, sx, 1);
+      sxx += __shfl_xor_sync(0xffffffffu, sxx, 1);
+    }
+    // the MMA: A fragments straight from the staged rows (a0: row g, k 2q..; a1: row g + 8; a2, a3: k + 8)
+    float acc[NT][4];
+#pragma unroll
+    for (int nt = 0; nt < NT; ++nt) acc[nt][0] = acc[nt][1] = acc[nt][2] = acc[nt][3] = 0.f;
+    {
+      const int g = lane / 4, q = lane % 4;
+      const unsigned char* r0 = rows + (size_t)g * pitch + 4 * q;
+      const unsigned char* r8 = rows + (size_t)(g + 8) * pitch + 4 * q;
+#pragma unroll
+      for (int ks = 0; ks < KMAX; ++ks) {
+        if (ks < KS) {
+          const uint32_t a0 = *(const uint32_t*)(r0 + ks * 32), a1 = *(const uint32_t*)(r8 + ks * 32);
+          const uint32_t a2 = *(const uint32_t*)(r0 + ks * 32 + 16), a3 = *(const uint32_t*)(r8 + ks * 32 + 16);
+#pragma unroll
+          for (int nt = 0; nt < NT; ++nt) {
+            if (std::is_same<T, __half>::value)
+              asm volatile(
+                  "mma.sync.aligned.m16n8k16.row.col.f32.f16.f16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+                  "{%0,%1,%2,%3};"
+                  : "+f"(acc[nt][0]), "+f"(acc[nt][1]), "+f"(acc[nt][2]), "+f"(acc[nt][3])
+                  : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(bf[ks][nt][0]), "r"(bf[ks][nt][1]));
+            else
+              asm volatile(
+                  "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+                  "{%0,%1,%2,%3};"
+                  : "+f"(acc[nt][0]), "+f"(acc[nt][1]), "+f"(acc[nt][2]), "+f"(acc[nt][3])
+                  : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(bf[ks][nt][0]), "r"(bf[ks][nt][1]));
+          }
+        }
+      }
+    }
+    __syncthreads();  // stage st read by every warp; the previous tile's outputs written
+    if (warp == 0 && tix + 2 * (int)gridDim.x < ntiles) issue(tix + 2 * gridDim.x, st);
+    // epilogue: rows g and g + 8 of the warp's 16, heads nt * 8 + 2q, + 1
+    {
+      const int g = lane / 4, q = lane % 4;
+      const float sx0 = __shfl_sync(0xffffffffu, sx, 2 * g), sxx0 = __shfl_sync(0xffffffffu, sxx, 2 * g);
+      const float sx8 = __shfl_sync(0xffffffffu, sx, 2 * (g + 8)), sxx8 = __shfl_sync(0xffffffffu, sxx, 2 * (g + 8));
+      const float m0 = sx0 * invC, m8 = sx8 * invC;
+      const float rs0 = rsqrtf(fmaxf(sxx0 * invC - m0 * m0, 0.f) + eps);
+      const float rs8 = rsqrtf(fmaxf(sxx8 * invC - m8 * m8, 0.f) + eps);
+#pragma unroll
+      for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int h = nt * 8 + 2 * q + e;
+          tile[h][warp * 16 + g] = rs0 * (acc[nt][e] - m0 * s1s[h]) + s2s[h];
+          tile[h][warp * 16 + g + 8] = rs8 * (acc[nt][2 + e] - m8 * s1s[h]) + s2s[h];
+        }
+    }
+    __syncthreads();
+    for (int t = threadIdx.x; t < H * TJ; t += blockDim.x) {
+      const int h = t / TJ, jo = t % TJ, j = jt * TJ + jo;
+      if (j < L) out[(((size_t)b * H + h) * L + i) * L + j] = evo::from_f<T>(tile[h][jo]);
     }
   }
 }
@@ -447,9 +625,33 @@ unsigned bwd_grid(const evo_pair_bias_desc* d) {  // one wave at the backward's 
 #ifndef EVO_PB_FR
 #define EVO_PB_FR 4  // forward rows per warp (a CTA covers 8 * EVO_PB_FR consecutive j)
 #endif
+#ifndef EVO_PB_MMA_CTAS
+#define EVO_PB_MMA_CTAS 8  // resident CTAs per SM of the tensor-pipe forward, at most (persistent)
+#endif
+#ifndef EVO_PB_MMA
+#define EVO_PB_MMA 1  // forward on the tensor pipe (mma.sync), else the shuffle-reduction kernel
+#endif
 template <typename T, int CPL, int HM>
 void launch_fwd(const evo_pair_bias_desc* d, const void* z, const float* g, const float* b, const float* w, void* out,
                 cudaStream_t st) {
+  if (EVO_PB_MMA) {
+    auto kern = pair_bias_fwd_mma_kernel<T, HM>;
+    const size_t shm = 2 * 64 * ((size_t)d->C * 2 + 16);
+    static int set = 0;
+    if ((int)shm > set) {
+      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shm);
+      set = (int)shm;
+    }
+    int per_sm = 1;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 128, shm);
+    const long long ntiles = d->Bo * d->L * ((d->L + 63) / 64);
+    // resident CTAs per SM: up to the occupancy limit, but >= ~4 tiles per CTA (the prologue builds the
+    // weight fragments) and <= EVO_PB_MMA_CTAS
+    const long long want = std::max<long long>(2, std::min<long long>(EVO_PB_MMA_CTAS, ntiles / (148LL * 4)));
+    const unsigned grid = (unsigned)std::min<long long>(ntiles, 148LL * std::min<long long>(std::max(per_sm, 1), want));
+    kern<<<grid, 128, shm, st>>>((const T*)z, g, b, w, (T*)out, (int)d->Bo, (int)d->L, (int)d->C, (int)d->H, d->eps);
+    return;
+  }
   constexpr int FR = EVO_PB_FR;
   auto kern = pair_bias_fwd_kernel<T, CPL, HM, FR>;
   const size_t shm = (size_t)CPL * HM * 32 * 4 + 2 * (size_t)kWarps * FR * d->C * sizeof(T);
