@@ -90,3 +90,44 @@ def test_simt_path_for_fp32():
 
     lib = N.load()
     assert lib.evo_attn_resolved_path(_desc(dtype=N.EVO_F32, dbias_dtype=N.EVO_F32)) == N.EVO_PATH_SIMT
+
+
+def _pb_desc(**kw):
+    from paper_2310_04610_b200 import _native as N
+
+    d = dict(Bo=1, L=64, C=128, H=8, dtype=N.EVO_BF16, dbias_dtype=N.EVO_F32, eps=1e-5)
+    d.update(kw)
+    return N.PairBiasDesc(**d)
+
+
+@pytest.mark.parametrize("kw,status", [
+    (dict(C=48), "UNSUPPORTED"),          # c_z not a multiple of 32
+    (dict(C=512), "UNSUPPORTED"),         # beyond the 256-channel envelope
+    (dict(H=17), "UNSUPPORTED"),
+    (dict(dtype=0), "VALIDATION"),        # z must be 16-bit
+    (dict(dbias_dtype=2), "VALIDATION"),  # f16 dBias with bf16 z
+    (dict(eps=0.0), "NUMERIC"),
+    (dict(L=0), "VALIDATION"),
+])
+def test_pair_bias_descriptor_validation(kw, status):
+    """The pair-bias projection's descriptor checks run before any device work (CPU only)."""
+    from paper_2310_04610_b200 import _native as N
+
+    lib = N.load()
+    d = _pb_desc(**kw)
+    st = lib.evo_pair_bias_fwd(C.byref(d), 1, 1, 1, 1, 1, None)
+    assert st == getattr(N, f"EVO_ERR_{status}"), lib.evo_attn_last_error()
+    assert lib.evo_pair_bias_bwd_workspace_size(C.byref(d)) == 0
+    assert lib.evo_pair_bias_fwd(None, 1, 1, 1, 1, 1, None) == N.EVO_ERR_USAGE
+
+
+def test_pair_bias_workspace_and_null_pointers():
+    from paper_2310_04610_b200 import _native as N
+
+    lib = N.load()
+    d = _pb_desc()
+    assert lib.evo_pair_bias_bwd_workspace_size(C.byref(d)) > 0
+    assert lib.evo_pair_bias_fwd(C.byref(d), None, 1, 1, 1, 1, None) == N.EVO_ERR_VALIDATION
+    ws = lib.evo_pair_bias_bwd_workspace_size(C.byref(d))
+    st = lib.evo_pair_bias_bwd(C.byref(d), 1, 1, 1, 1, 1, 1, 1, 1, 1, 1, ws - 1, None)
+    assert st == N.EVO_ERR_VALIDATION  # workspace smaller than required
