@@ -31,7 +31,10 @@ namespace tc {
 
 constexpr int kBM = 128;                 // query rows per tile (UMMA M, TMEM lanes)
 constexpr int kBN = 64;                  // keys per tile (UMMA N of S)
-constexpr float kRescaleThreshold = 8.f;  // log2 units
+#ifndef EVO_FWD_RESCALE_LOG2
+#define EVO_FWD_RESCALE_LOG2 8  // lazy rescale once the running max grew by more than this (log2 units)
+#endif
+constexpr float kRescaleThreshold = (float)EVO_FWD_RESCALE_LOG2;
 #ifndef EVO_FWD_POLY_EVERY
 #define EVO_FWD_POLY_EVERY 4
 #endif
