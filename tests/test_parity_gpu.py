@@ -123,7 +123,10 @@ def test_launches_counted():
     q, k, v, do, b1, b2 = make_inputs(1, 2, 64, 2, 32)
     t = lambda a: torch.tensor(a, dtype=torch.bfloat16, device="cuda")
     o, lse = E.evoformer_attention_forward(t(q), t(k), t(v), t(b1), t(b2))
-    assert E.last_launch_count() >= 1
+    assert E.resolved_path(t(q), t(b1), t(b2)) == "tcgen05"
+    assert E.last_launch_count() == 1  # K1 alone
+    E.evoformer_attention_backward(t(do), t(q), t(k), t(v), o, lse, t(b1), t(b2))
+    assert E.last_launch_count() == 3  # preamble, K3, dQ conversion
 
 
 def test_validation_errors_map_to_taxonomy():
